@@ -1,0 +1,160 @@
+/*
+ * flashsample.h -- C ABI of the B200-native FlashSampling hot path
+ * (arXiv 2603.15854, "FlashSampling: exact sampling fused into the LM-head matmul").
+ *
+ * The library computes, for every batch row b, one exact sample of
+ *     Cat(softmax(l~_b)),   l~_{b,v} = transform( sum_d h[b,d] * W[v,d] )
+ * as  idx_b = argmax_v ( l~_{b,v} + g_{b,v} ),  g ~ Gumbel(0,1)
+ * (Gumbel-Max theorem; fused two-stage Alg. 2), with the
+ * [B,V] logits never written to HBM.  "P:n" = line n of PAPER.md.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  Layout      h [B,D] row-major, W [V,D] row-major (nn.Linear weight), both K(=D)-major.
+ *              bf16 (FS_BF16) or fp32 (FS_F32).  fp32 is computed with true fp32 FMA on
+ *              CUDA cores (never TF32); bf16 on tcgen05 tensor cores with fp32 accumulation
+ *              (P:199-202).
+ *  Transform   l~ = (acc + bias[v]) * (1/temperature[b]); mask bit 0 -> -inf; NaN -> -inf
+ *              (Alg. 2 line 9 P:169, masking §4.6; order = DESIGN.md reading R3).
+ *              bias      [V] fp32 or NULL (= 0)
+ *              temperature [B] fp32 or NULL (= 1); a row with tau <= 0 or non-finite is undefined
+ *              mask      [B][mask_words] uint32, bit (v & 31) of word (v >> 5) = 1 -> token v allowed;
+ *                        NULL = all allowed.  mask_words = ceil(V_total/32); ids are GLOBAL ids.
+ *  RNG         Philox4x32-10, key = (seed lo, seed hi), counter = (v_global, b>>2, step lo,
+ *              (step hi & 0xFFFFFF) | tag<<24), r = out[b & 3]; u = (r+1)/(2^32+1);
+ *              g = -log(-log u) evaluated tail-accurately in fp32 (App. C P:849-853;
+ *              DESIGN.md readings R1, R2).  Results are a deterministic function of
+ *              (inputs, seed, step): independent of tiling, grid, shard count or stream.
+ *  Ties        equal perturbed scores resolve to the smallest global vocabulary id (reading R5).
+ *  Undefined   a row with no finite l~ (all masked, or invalid tau) yields idx = -1,
+ *              score = -inf, log-mass = -inf ("undefined"; reading R7).  Never an error.
+ *  Indices     0-based global vocabulary ids (int32).
+ *  Memory      every pointer argument except ctx is a DEVICE pointer owned by the caller,
+ *              16-byte aligned for h and W; the library never frees or retains them after the
+ *              call returns.  The library owns only fs_ctx (workspace, tensor-map cache).
+ *  Streams     `stream` is a cudaStream_t (NULL = legacy default stream).  All calls are
+ *              asynchronous on it, perform no host synchronisation and, once the workspace has
+ *              grown for a shape, no allocation: they are CUDA-graph capturable.
+ *  Errors      synchronous status for anything checkable on the host (fs_status); the
+ *              message of the last failure on the calling thread is fs_last_error().
+ *  Limits      1 <= B (rows are processed in chunks of at most 256 per launch),
+ *              1 <= D, 1 <= V < 2^31, bf16 tensor-core path needs D % 8 == 0 (TMA row stride);
+ *              other D fall back to the CUDA-core kernel (same results, slower).
+ */
+#ifndef FLASHSAMPLE_H
+#define FLASHSAMPLE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FS_OK = 0,
+  FS_ERR_INVALID = 1,      /* bad argument (NULL required pointer, size < 1, misalignment, ...) */
+  FS_ERR_UNSUPPORTED = 2,  /* valid but not supported by this build (e.g. no sm_100 device)    */
+  FS_ERR_CUDA = 3,         /* a CUDA runtime / driver call failed (message in fs_last_error)   */
+  FS_ERR_OOM = 4           /* workspace allocation failed                                      */
+} fs_status;
+
+typedef enum { FS_BF16 = 0, FS_F32 = 1 } fs_dtype;
+
+/* Group / shard summary (Lemma "max-stability"; Alg. A.4 message P:830):
+ *   max_score = M_k = max_{v in G_k} (l~_v + g_v)     (-inf if the group has no finite l~)
+ *   idx       = I_k = smallest global id attaining M_k (-1 if empty)
+ *   log_mass  = L_k = log sum_{v in G_k} exp(l~_v)   (-inf if empty)              12 bytes. */
+typedef struct {
+  float max_score;
+  int32_t idx;
+  float log_mass;
+} fs_summary;
+
+typedef struct fs_ctx fs_ctx;
+
+/* Version string of the library build. */
+const char* fs_version(void);
+const char* fs_status_str(fs_status s);
+/* Message of the last failing call on this thread ("" if none). */
+const char* fs_last_error(void);
+
+/* Create a context bound to CUDA device `device` (workspace, tensor-map cache, SM count).
+ * Fails with FS_ERR_UNSUPPORTED if the device is not compute capability 10.0 (B200). */
+fs_status fs_ctx_create(int device, fs_ctx** out);
+void fs_ctx_destroy(fs_ctx* ctx);
+/* Testing / tuning knobs: force the CUDA-core kernel (1) or the tcgen05 kernel (0, default);
+ * cap the persistent grid at `max_ctas` (0 = number of SMs). */
+fs_status fs_ctx_set_option(fs_ctx* ctx, const char* name, int64_t value);
+
+/* fs_sample -- fused LM-head projection + exact Gumbel-max sampling (Alg. 2).
+ *   h [B,D], W [V,D] (dtype), bias/temperature/mask as above (mask_words = ceil(V/32)).
+ *   idx_out   [B] int32 (required): sampled global vocabulary id, -1 for undefined rows.
+ *   score_out [B] fp32 or NULL: the winning perturbed score max_v (l~_v + g_v).
+ * Workload per call: W is streamed from HBM exactly once; only per-CTA candidates
+ * (B x #CTA x 16 bytes) are written besides the outputs. */
+fs_status fs_sample(fs_ctx* ctx, fs_dtype dtype,
+                    const void* h, const void* W,
+                    const float* bias, const float* temperature, const uint32_t* mask,
+                    uint64_t seed, uint64_t step, int B, int D, int V,
+                    int32_t* idx_out, float* score_out, void* stream);
+
+/* fs_sample_grouped -- grouped / online FlashSampling with per-group log-mass summaries
+ * (Group-Gumbel-Max §4.1, Alg. A.2/A.3 P:768-815, log-normalizer App. E).
+ * Groups are contiguous vocabulary ranges G_k = [k*g, min((k+1)*g, V)), k = 0..ceil(V/g)-1,
+ * g = group_size, a multiple of 128 (last group ragged).  The outer selection reuses the
+ * group maxima (reading R8), so idx_out equals fs_sample's idx_out exactly.
+ *   logZ_out   [B] fp32 or NULL: log sum_v exp(l~_v) = logsumexp_k L_k.
+ *   groups_out [B][ceil(V/g)] fs_summary or NULL. */
+fs_status fs_sample_grouped(fs_ctx* ctx, fs_dtype dtype,
+                            const void* h, const void* W,
+                            const float* bias, const float* temperature, const uint32_t* mask,
+                            uint64_t seed, uint64_t step, int B, int D, int V, int group_size,
+                            int32_t* idx_out, float* score_out, float* logZ_out,
+                            fs_summary* groups_out, void* stream);
+
+/* fs_sample_shard -- the rank-local half of distributed FlashSampling for a vocabulary-
+ * sharded (tensor-parallel) LM head (§4.2, Alg. A.4).
+ *   W_shard [V_local,D] holds global rows [vocab_offset, vocab_offset+V_local);
+ *   bias_shard [V_local] or NULL; mask is the GLOBAL bitmask [B][ceil(V_total/32)] or NULL;
+ *   the RNG is keyed by global ids, so the union of shards reproduces fs_sample on the
+ *   full matrix bit-for-bit.
+ *   summary_out [B] fs_summary (required): this shard's (M, I, L) per row -- the 12-byte
+ *   message every rank contributes to the all-gather. */
+fs_status fs_sample_shard(fs_ctx* ctx, fs_dtype dtype,
+                          const void* h, const void* W_shard,
+                          const float* bias_shard, const float* temperature, const uint32_t* mask,
+                          uint64_t seed, uint64_t step, int B, int D, int V_local,
+                          int64_t vocab_offset, int64_t V_total,
+                          fs_summary* summary_out, void* stream);
+
+/* fs_combine_summaries -- outer selection over n gathered shard/group summaries
+ * (Alg. A.4 lines 5-7, with max reuse P:286): for each row,
+ *   idx = I_{k*}, k* = argmax_k M_k (ties -> smaller global id), score = M_{k*},
+ *   logZ = logsumexp_k L_k.
+ *   gathered [n][B] fs_summary (device); idx_out [B] required; score_out, logZ_out optional. */
+fs_status fs_combine_summaries(const fs_summary* gathered, int n, int B,
+                               int32_t* idx_out, float* score_out, float* logZ_out,
+                               void* stream);
+
+/* fs_merge_summaries -- online binary merge of two summaries of disjoint vocabulary sets
+ * (Alg. A.3, Lemma "binary merge" P:315-349, realised by max reuse):
+ *   out.max_score = max, out.idx = idx of the max (ties -> smaller id),
+ *   out.log_mass = logaddexp(a.log_mass, b.log_mass).  Associative and commutative.
+ *   a, b, out: [count] device arrays (out may alias a or b). */
+fs_status fs_merge_summaries(const fs_summary* a, const fs_summary* b, fs_summary* out,
+                             int count, void* stream);
+
+/* Diagnostics (used by the tests to pin the device RNG; not on the hot path).
+ * fs_random_bits: r[i] = Philox draw for (b[i], v[i]) under (seed, step, tag) -- the exact
+ *                 counter layout of the convention above.  All arrays device, length n.
+ * fs_gumbel_from_bits: g[i] = device fp32 G32(r[i]). */
+fs_status fs_random_bits(uint64_t seed, uint64_t step, uint32_t tag,
+                         const int32_t* b, const int64_t* v, uint32_t* r_out, int64_t n,
+                         void* stream);
+fs_status fs_gumbel_from_bits(const uint32_t* r, float* g_out, int64_t n, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FLASHSAMPLE_H */

@@ -1,0 +1,210 @@
+"""FlashSampling on B200: fused LM-head projection + exact Gumbel-max sampling (arXiv 2603.15854).
+
+Thin Python binding over the C ABI (include/flashsample.h, libflashsample.so).  Every step
+of the sampling path runs in the library's sm_100a kernels; this module only validates
+tensors, passes pointers and the current CUDA stream, and allocates outputs.
+
+    import paper_2603_15854_b200 as fs
+    idx = fs.sample(h, W, seed=..., step=...)                       # Alg. 2
+    idx, logZ, groups = fs.sample_grouped(h, W, group_size=4096)    # §4.1, App. E
+    summ = fs.sample_shard(h, W_shard, vocab_offset, V_total)       # Alg. A.4 rank-local half
+    idx = fs.combine_summaries(gathered)                            # Alg. A.4 outer selection
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+
+import torch
+
+from . import _lib
+from ._lib import FS_BF16, FS_F32, FlashSampleError
+
+__all__ = ["sample", "sample_grouped", "sample_shard", "combine_summaries", "merge_summaries",
+           "random_bits", "gumbel_from_bits", "Summaries", "context", "set_option",
+           "FlashSampleError", "version", "sample_from_host"]
+
+_ctx = {}
+
+
+def version() -> str:
+    return _lib.lib().fs_version().decode()
+
+
+def context(device: int | torch.device | None = None) -> int:
+    """The library context (ctypes handle) for a CUDA device, created on first use."""
+    if device is None:
+        device = torch.cuda.current_device()
+    if isinstance(device, torch.device):
+        device = device.index if device.index is not None else torch.cuda.current_device()
+    if device not in _ctx:
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib().fs_ctx_create(int(device), ctypes.byref(h)), "fs_ctx_create")
+        _ctx[device] = h
+    return _ctx[device]
+
+
+def set_option(name: str, value: int, device=None) -> None:
+    _lib.check(_lib.lib().fs_ctx_set_option(context(device), name.encode(), int(value)), "fs_ctx_set_option")
+
+
+def _stream(t: torch.Tensor):
+    return ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _dtype_code(h: torch.Tensor, W: torch.Tensor) -> int:
+    if h.dtype != W.dtype:
+        raise TypeError("h and W must have the same dtype")
+    if h.dtype == torch.bfloat16:
+        return FS_BF16
+    if h.dtype == torch.float32:
+        return FS_F32
+    raise TypeError(f"unsupported dtype {h.dtype} (bf16 or fp32)")
+
+
+def _check_inputs(h, W, bias, temperature, mask, V_total=None):
+    for name, t in (("h", h), ("W", W)):
+        if not t.is_cuda or not t.is_contiguous() or t.dim() != 2:
+            raise ValueError(f"{name} must be a contiguous 2-D CUDA tensor")
+    B, D = h.shape
+    V, D2 = W.shape
+    if D != D2:
+        raise ValueError("h and W disagree on D")
+    V_total = V if V_total is None else V_total
+    if bias is not None and (bias.dtype != torch.float32 or bias.numel() != V or not bias.is_contiguous()):
+        raise ValueError("bias must be a contiguous fp32 [V] tensor")
+    if temperature is not None and (temperature.dtype != torch.float32 or temperature.numel() != B
+                                    or not temperature.is_contiguous()):
+        raise ValueError("temperature must be a contiguous fp32 [B] tensor")
+    if mask is not None and (mask.dtype != torch.int32 or tuple(mask.shape) != (B, (V_total + 31) // 32)
+                             or not mask.is_contiguous()):
+        raise ValueError("mask must be a contiguous int32 [B, ceil(V/32)] bit tensor")
+    return B, D, V
+
+
+def sample(h, W, *, bias=None, temperature=None, mask=None, seed: int = 0, step: int = 0,
+           return_score: bool = False, out=None):
+    """Fused LM-head + exact Gumbel-max sample per row (fs_sample).  Returns int32 [B]
+    (and the winning perturbed scores, fp32 [B], if return_score)."""
+    B, D, V = _check_inputs(h, W, bias, temperature, mask)
+    idx = out if out is not None else torch.empty(B, dtype=torch.int32, device=h.device)
+    score = torch.empty(B, dtype=torch.float32, device=h.device) if return_score else None
+    _lib.check(_lib.lib().fs_sample(context(h.device), _dtype_code(h, W), _ptr(h), _ptr(W), _ptr(bias),
+                                    _ptr(temperature), _ptr(mask), seed & (2**64 - 1), step & (2**64 - 1),
+                                    B, D, V, _ptr(idx), _ptr(score), _stream(h)), "fs_sample")
+    return (idx, score) if return_score else idx
+
+
+@dataclasses.dataclass
+class Summaries:
+    """fs_summary records {max_score f32, idx i32, log_mass f32} stored as int32 [..., 3]."""
+    raw: torch.Tensor
+
+    @property
+    def max_score(self):
+        return self.raw[..., 0].view(torch.float32)
+
+    @property
+    def idx(self):
+        return self.raw[..., 1]
+
+    @property
+    def log_mass(self):
+        return self.raw[..., 2].view(torch.float32)
+
+    @staticmethod
+    def empty(*shape, device):
+        return Summaries(torch.empty(*shape, 3, dtype=torch.int32, device=device))
+
+
+def sample_grouped(h, W, *, group_size: int, bias=None, temperature=None, mask=None, seed: int = 0,
+                   step: int = 0, return_groups: bool = True):
+    """Grouped FlashSampling (fs_sample_grouped).  Returns (idx [B] int32, score [B] fp32,
+    logZ [B] fp32, Summaries [B, ceil(V/g)] or None)."""
+    B, D, V = _check_inputs(h, W, bias, temperature, mask)
+    n_groups = (V + group_size - 1) // group_size
+    idx = torch.empty(B, dtype=torch.int32, device=h.device)
+    score = torch.empty(B, dtype=torch.float32, device=h.device)
+    logZ = torch.empty(B, dtype=torch.float32, device=h.device)
+    groups = Summaries.empty(B, n_groups, device=h.device) if return_groups else None
+    _lib.check(_lib.lib().fs_sample_grouped(
+        context(h.device), _dtype_code(h, W), _ptr(h), _ptr(W), _ptr(bias), _ptr(temperature), _ptr(mask),
+        seed & (2**64 - 1), step & (2**64 - 1), B, D, V, group_size, _ptr(idx), _ptr(score), _ptr(logZ),
+        _ptr(groups.raw) if groups else None, _stream(h)), "fs_sample_grouped")
+    return idx, score, logZ, groups
+
+
+def sample_shard(h, W_shard, vocab_offset: int, V_total: int, *, bias_shard=None, temperature=None,
+                 mask=None, seed: int = 0, step: int = 0, out: Summaries | None = None) -> Summaries:
+    """Rank-local half of distributed FlashSampling (fs_sample_shard): this shard's (M, I, L)."""
+    B, D, V = _check_inputs(h, W_shard, bias_shard, temperature, mask, V_total=V_total)
+    summ = out if out is not None else Summaries.empty(B, device=h.device)
+    _lib.check(_lib.lib().fs_sample_shard(
+        context(h.device), _dtype_code(h, W_shard), _ptr(h), _ptr(W_shard), _ptr(bias_shard), _ptr(temperature),
+        _ptr(mask), seed & (2**64 - 1), step & (2**64 - 1), B, D, V, int(vocab_offset), int(V_total),
+        _ptr(summ.raw), _stream(h)), "fs_sample_shard")
+    return summ
+
+
+def combine_summaries(gathered: Summaries | torch.Tensor, *, return_all: bool = False):
+    """Outer selection over gathered summaries [n, B] (fs_combine_summaries)."""
+    raw = gathered.raw if isinstance(gathered, Summaries) else gathered
+    n, B = raw.shape[0], raw.shape[1]
+    raw = raw.contiguous()
+    idx = torch.empty(B, dtype=torch.int32, device=raw.device)
+    score = torch.empty(B, dtype=torch.float32, device=raw.device)
+    logZ = torch.empty(B, dtype=torch.float32, device=raw.device)
+    _lib.check(_lib.lib().fs_combine_summaries(_ptr(raw), n, B, _ptr(idx), _ptr(score), _ptr(logZ),
+                                               _stream(raw)), "fs_combine_summaries")
+    return (idx, score, logZ) if return_all else idx
+
+
+def merge_summaries(a: Summaries, b: Summaries) -> Summaries:
+    """Online binary merge of two summary arrays of disjoint vocabularies (fs_merge_summaries)."""
+    out = Summaries(torch.empty_like(a.raw))
+    _lib.check(_lib.lib().fs_merge_summaries(_ptr(a.raw.contiguous()), _ptr(b.raw.contiguous()), _ptr(out.raw),
+                                             a.raw.numel() // 3, _stream(a.raw)), "fs_merge_summaries")
+    return out
+
+
+def random_bits(seed: int, step: int, b: torch.Tensor, v: torch.Tensor, tag: int = 0) -> torch.Tensor:
+    """Device Philox draws r for positions (b[i], v[i]) (diagnostic, fs_random_bits)."""
+    b = b.to(torch.int32).contiguous()
+    v = v.to(torch.int64).contiguous()
+    r = torch.empty(b.numel(), dtype=torch.int32, device=b.device)
+    _lib.check(_lib.lib().fs_random_bits(seed & (2**64 - 1), step & (2**64 - 1), tag, _ptr(b), _ptr(v), _ptr(r),
+                                         b.numel(), _stream(b)), "fs_random_bits")
+    return r
+
+
+def gumbel_from_bits(r: torch.Tensor) -> torch.Tensor:
+    """Device fp32 G32(r) (diagnostic, fs_gumbel_from_bits).  r: int32 tensor of bit patterns."""
+    r = r.contiguous()
+    g = torch.empty(r.shape, dtype=torch.float32, device=r.device)
+    _lib.check(_lib.lib().fs_gumbel_from_bits(_ptr(r), _ptr(g), r.numel(), _stream(r)), "fs_gumbel_from_bits")
+    return g
+
+
+def sample_from_host(h_host, W, *, temperature_host=None, mask_host=None, bias=None, seed=0, step=0,
+                     h_dev=None, t_dev=None, m_dev=None, idx_dev=None, idx_host=None):
+    """End-to-end call a serving loop makes: copy this step's inputs from (pinned) host memory,
+    sample on the device, copy the sampled ids back.  Device staging buffers may be passed in
+    to avoid allocation.  Returns the host int32 [B] tensor."""
+    dev = W.device
+    h_dev = h_dev if h_dev is not None else torch.empty_like(h_host, device=dev)
+    h_dev.copy_(h_host, non_blocking=True)
+    if temperature_host is not None:
+        t_dev = t_dev if t_dev is not None else torch.empty_like(temperature_host, device=dev)
+        t_dev.copy_(temperature_host, non_blocking=True)
+    if mask_host is not None:
+        m_dev = m_dev if m_dev is not None else torch.empty_like(mask_host, device=dev)
+        m_dev.copy_(mask_host, non_blocking=True)
+    idx_dev = sample(h_dev, W, bias=bias, temperature=t_dev if temperature_host is not None else None,
+                     mask=m_dev if mask_host is not None else None, seed=seed, step=step, out=idx_dev)
+    idx_host = idx_host if idx_host is not None else torch.empty(idx_dev.shape, dtype=torch.int32, pin_memory=True)
+    idx_host.copy_(idx_dev, non_blocking=True)
+    return idx_host

@@ -1,0 +1,142 @@
+// fs_device.cuh -- per-element arithmetic of the fused epilogue (sm_100a).
+//
+// Philox4x32-10, the tail-accurate fp32 Gumbel map G32, the order-preserving score key and
+// the running (key, idx, S) state used by both stage-1 kernels (tcgen05 and CUDA-core) and
+// by the reduction kernels.  See include/flashsample.h for the conventions and DESIGN.md
+// for the readings R1-R8 of PAPER.md.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fs {
+
+// ---------------------------------------------------------------------------------------
+// Philox4x32-10 ("counter-based RNG (e.g. Philox)"; reading R1).
+// ---------------------------------------------------------------------------------------
+constexpr uint32_t kPhiloxM0 = 0xD2511F53u;
+constexpr uint32_t kPhiloxM1 = 0xCD9E8D57u;
+constexpr uint32_t kPhiloxW0 = 0x9E3779B9u;
+constexpr uint32_t kPhiloxW1 = 0xBB67AE85u;
+
+struct U4 { uint32_t x, y, z, w; };
+
+__device__ __forceinline__ U4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                            uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(kPhiloxM0, c0), lo0 = kPhiloxM0 * c0;
+    const uint32_t hi1 = __umulhi(kPhiloxM1, c2), lo1 = kPhiloxM1 * c2;
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+    k0 += kPhiloxW0; k1 += kPhiloxW1;
+  }
+  return U4{c0, c1, c2, c3};
+}
+
+// Counter words 2 and 3 for (step, tag).
+__device__ __forceinline__ uint32_t ctr_step_lo(uint64_t step) { return (uint32_t)step; }
+__device__ __forceinline__ uint32_t ctr_step_hi(uint64_t step, uint32_t tag) {
+  return ((uint32_t)(step >> 32) & 0x00FFFFFFu) | (tag << 24);
+}
+
+// ---------------------------------------------------------------------------------------
+// G32(r) = -log(-log u), u = (r+1)/(2^32+1)   (App. C; reading R2).
+// fp32 with MUFU lg2 only where the result's absolute error is bounded:
+//   r <  2^31 : u = (r+1)*2^-32 (1/(2^32+1) rounds to 2^-32 in fp32), E = -ln u >= ln 2,
+//               so the abs error of ln u (~2^-22) is a small relative error of E.
+//   r >= 2^31 : w = (2^32 - r)*2^-32 = 1 - u <= 1/2, E = -log1p(-w) = 2 atanh(s),
+//               s = w/(2-w) <= 1/3, by the odd series 2 s (1 + s^2/3 + ... + s^14/15)
+//               (truncation < 1.5e-8 relative), so E keeps full relative accuracy
+//               even for w ~ 2^-32.
+//   g = -ln E.   Budget |G32 - G64| <= 1e-5 (exhaustive test in tests/test_gpu_rng.py).
+// Branch-free: both forms are evaluated and selected, which costs the same as the
+// divergent branch in a warp and keeps the epilogue convergent.
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ float fast_log2(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float fast_rcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+constexpr float kLn2 = 0.69314718055994530942f;
+constexpr float kLog2e = 1.44269504088896340736f;
+constexpr float kTwoM32 = 2.3283064365386963e-10f;   // 2^-32
+
+__device__ __forceinline__ float gumbel32(uint32_t r) {
+  // lower branch: E = -ln u = (32 - log2(r+1)) * ln2
+  const float x_lo = (float)(r + 1u);                                // used only for r < 2^31
+  const float E_lo = (32.0f - fast_log2(x_lo)) * kLn2;
+  // upper branch: w = (2^32 - r) 2^-32, s = w/(2-w), E = 2 s P(s^2)
+  const float w = (float)(0u - r) * kTwoM32;                         // 2^32 - r for r >= 2^31
+  const float den = 2.0f - w;
+  float s = w * fast_rcp(den);
+  s = fmaf(fmaf(-s, den, w), fast_rcp(den), s);                      // one Newton step
+  const float t = s * s;
+  float p = 1.0f / 15.0f;
+  p = fmaf(p, t, 1.0f / 13.0f);
+  p = fmaf(p, t, 1.0f / 11.0f);
+  p = fmaf(p, t, 1.0f / 9.0f);
+  p = fmaf(p, t, 1.0f / 7.0f);
+  p = fmaf(p, t, 1.0f / 5.0f);
+  p = fmaf(p, t, 1.0f / 3.0f);
+  p = fmaf(p, t, 1.0f);
+  const float E_hi = 2.0f * s * p;
+  const float E = (r < 0x80000000u) ? E_lo : E_hi;
+  return -fast_log2(E) * kLn2;
+}
+
+// ---------------------------------------------------------------------------------------
+// Order-preserving key: float order == uint32 order (for non-NaN inputs).
+// ---------------------------------------------------------------------------------------
+__device__ __host__ __forceinline__ uint32_t order_key_bits(uint32_t x) {
+  return x ^ ((x & 0x80000000u) ? 0xFFFFFFFFu : 0x80000000u);
+}
+__device__ __forceinline__ uint32_t order_key(float f) { return order_key_bits(__float_as_uint(f)); }
+__device__ __forceinline__ float key_to_float(uint32_t k) {
+  const uint32_t x = (k & 0x80000000u) ? (k ^ 0x80000000u) : ~k;
+  return __uint_as_float(x);
+}
+// key(-inf) = ~0xFF800000; key 0 marks "no element" (out-of-range rows), below every score.
+constexpr uint32_t kKeyNegInf = 0x007FFFFFu;
+constexpr uint32_t kKeyNone = 0u;
+
+// Running state of a (row, vocabulary range): best key, its smallest global id, and the
+// log-mass S = sum exp(l~ - M) relative to M = key_to_float(key) (App. E).
+struct State {
+  uint32_t key;
+  int32_t idx;
+  float S;
+  uint32_t pad;
+};
+
+__device__ __forceinline__ State state_empty() { return State{kKeyNone, -1, 0.0f, 0u}; }
+
+__device__ __forceinline__ float key_ref(uint32_t key) {
+  return key > kKeyNegInf ? key_to_float(key) : -INFINITY;
+}
+
+// Merge two states over disjoint vocabulary sets: max-merge (ties -> smaller id) and
+// logaddexp of the masses (binary merge realised by max reuse).
+__device__ __forceinline__ State state_merge(State a, State b) {
+  const bool take_b = (b.key > a.key) || (b.key == a.key && b.idx >= 0 && (a.idx < 0 || b.idx < a.idx));
+  State hi = take_b ? b : a;
+  const State lo = take_b ? a : b;
+  const float mh = key_ref(hi.key), ml = key_ref(lo.key);
+  float S = hi.S;
+  if (lo.S > 0.0f && ml != -INFINITY && mh != -INFINITY) S += lo.S * fast_exp2((ml - mh) * kLog2e);
+  else if (mh == -INFINITY) S = 0.0f;
+  hi.S = S;
+  return hi;
+}
+
+}  // namespace fs

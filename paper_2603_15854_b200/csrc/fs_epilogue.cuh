@@ -1,0 +1,125 @@
+// fs_epilogue.cuh -- the fused epilogue of Alg. 2 shared by the tcgen05
+// stage-1 kernel and the CUDA-core stage-1 kernel.
+//
+// Thread <-> data mapping (swap-AB): one thread owns one vocabulary row v (a TMEM lane), a warp
+// owns 32 consecutive rows; the accumulator columns are the batch rows b.  For each column b:
+//   l~ = (acc + bias_v) * invtau_b, banned / NaN -> -inf          (Alg. 2 line 9; §4.6)
+//   g  = G32(Philox(v, b>>2, step)[b&3])                           (line 10; App. C)
+//   s  = l~ + g, key = order-preserving uint32 of s               (line 11)
+//   warp max of key (redux.sync) + ballot -> smallest winning lane (= smallest v, reading R5)
+//   lane (b mod 32) folds (kmax, v_win[, S_w]) into its running State for column b (line 14).
+// With LSE the warp also sums exp(l~ - M_w) (App. E), M_w = warp max perturbed score:
+// since -3.10 <= g <= 22.19, every l~ - M_w <= 3.1 and the max term is >= e^-22.2, so the
+// fp32 sum neither overflows nor underflows (reading R9).
+#pragma once
+#include "fs_device.cuh"
+#include "fs_sm100.cuh"
+
+namespace fs {
+
+struct EpiArgs {
+  const float* invtau;      // smem [BN]: 1/tau_b, NaN for invalid or padding columns
+  const uint32_t* mask;     // global [rows][mask_words] for this launch's rows, or nullptr
+  int64_t mask_words;
+  int B;                    // valid columns in this launch
+  int row_offset;           // global batch index of column 0 (RNG counter)
+  uint32_t k0, k1, c2, c3;  // Philox key and counter words 2, 3
+};
+
+struct RowArgs {
+  bool valid;               // this lane's vocabulary row is inside the tile
+  uint32_t v_lo;            // low word of the global vocabulary id (Philox counter word 0)
+  int32_t v_global;         // global vocabulary id
+  int32_t warp_v0;          // global id of lane 0's row (rows of a warp are consecutive)
+  float bias;
+};
+
+// Fold the warp result for one column into the owning lane's running state.  Tiles reach a
+// warp in increasing vocabulary order, so a strictly larger key wins and an equal key keeps
+// the earlier (smaller) id.
+template <bool LSE>
+__device__ __forceinline__ void absorb(State& own, uint32_t kmax, int32_t widx, float S_w) {
+  if (kmax > own.key) {
+    if (LSE) {
+      const float m_old = key_ref(own.key), m_new = key_ref(kmax);
+      own.S = (own.key > kKeyNegInf ? own.S * fast_exp2((m_old - m_new) * kLog2e) : 0.0f) + S_w;
+    }
+    own.key = kmax;
+    own.idx = widx;
+  } else if (LSE) {
+    if (kmax > kKeyNegInf) own.S += S_w * fast_exp2((key_ref(kmax) - key_ref(own.key)) * kLog2e);
+  }
+}
+
+// Process NCOL (multiple of 4) consecutive accumulator columns [col0, col0+NCOL) of this lane's
+// row; `own` is this lane's state for column col0 + lane.
+template <int NCOL, bool LSE>
+__device__ __forceinline__ void epi_columns(const float* acc, int col0, const RowArgs& ra,
+                                            const EpiArgs& ea, State& own, int lane) {
+#pragma unroll
+  for (int j = 0; j < NCOL; j += 4) {
+    const int b0 = col0 + j;
+    if (b0 >= ea.B) break;                                   // warp-uniform
+    const U4 r4 = philox4x32_10(ra.v_lo, (uint32_t)(ea.row_offset + b0) >> 2, ea.c2, ea.c3, ea.k0, ea.k1);
+    const uint32_t rr[4] = {r4.x, r4.y, r4.z, r4.w};
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int b = b0 + jj;
+      float lt = (acc[j + jj] + ra.bias) * ea.invtau[b];
+      if (ea.mask != nullptr && b < ea.B) {
+        const uint32_t w = __ldg(ea.mask + (int64_t)b * ea.mask_words + (ra.v_global >> 5));
+        if (!((w >> (ra.v_global & 31)) & 1u)) lt = -INFINITY;
+      }
+      if (isnan(lt)) lt = -INFINITY;
+      const float s = lt + gumbel32(rr[jj]);
+      const uint32_t key = ra.valid ? order_key(s) : kKeyNone;
+      const uint32_t kmax = __reduce_max_sync(0xFFFFFFFFu, key);
+      const uint32_t ball = __ballot_sync(0xFFFFFFFFu, key == kmax);
+      const int32_t widx = kmax > kKeyNone ? ra.warp_v0 + (__ffs(ball) - 1) : -1;
+      float S_w = 0.0f;
+      if (LSE) {
+        const float m = key_ref(kmax);
+        float e = (ra.valid && m != -INFINITY) ? fast_exp2((lt - m) * kLog2e) : 0.0f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xFFFFFFFFu, e, o);
+        S_w = e;
+      }
+      if (lane == ((j + jj) & 31)) absorb<LSE>(own, kmax, widx, S_w);
+    }
+  }
+}
+
+// Merge the per-warp states of the 4 TMEM lane quadrants (one epilogue warp each) for every
+// column and write one candidate per column to `part_row` (Alg. 2 line 15).
+template <int NCHUNK, int COLS_PER_CHUNK>
+__device__ __forceinline__ void flush_states(State (&st)[NCHUNK], State* scratch, int BN, int q, int lane,
+                                             int epi_tid, int B, State* part_row, uint32_t bar_id) {
+#pragma unroll
+  for (int c = 0; c < NCHUNK; ++c) {
+    if (lane < COLS_PER_CHUNK) scratch[q * BN + c * COLS_PER_CHUNK + lane] = st[c];
+    st[c] = state_empty();
+  }
+  sm100::named_bar_sync(bar_id, 128);
+  for (int b = epi_tid; b < B; b += 128) {
+    State m = scratch[b];
+#pragma unroll
+    for (int qq = 1; qq < 4; ++qq) m = state_merge(m, scratch[qq * BN + b]);
+    part_row[b] = m;
+  }
+  sm100::named_bar_sync(bar_id, 128);
+}
+
+// Persistent-CTA vocabulary partition: CTA c of G owns rows [16*floor(c*U/G), 16*floor((c+1)*U/G))
+// (U = ceil(V/16) 16-row units), clipped to V.  Balanced to one 16-row unit, so no CTA streams
+// more than ceil(U/G)*16 rows of W (no split-K, so every logit's fp32 sum is independent of G).
+__device__ __forceinline__ void cta_rows(int cta, int G, int V, int& r0, int& r1) {
+  const int64_t U = (V + 15) / 16;
+  r0 = (int)(16 * ((int64_t)cta * U / G));
+  const int64_t e = 16 * ((int64_t)(cta + 1) * U / G);
+  r1 = (int)(e < (int64_t)V ? e : (int64_t)V);
+}
+// Tiles are the intersections of the CTA's rows with 128-aligned blocks, so a tile never
+// straddles a group boundary (group sizes are multiples of 128).
+__device__ __forceinline__ int tile_end(int t0, int r1) { return min(r1, (t0 & ~127) + 128); }
+
+}  // namespace fs

@@ -1,0 +1,158 @@
+// fs_reduce.cu -- stage 2 of FlashSampling and the summary kernels.
+//
+//  reduce   Alg. 2 stage 2: per row, argmax over the per-CTA candidates
+//           (ties -> smaller id); in grouped mode first merges the candidates of each group into
+//           (M_k, I_k, L_k) (§4.1, Lemma P:254-270) and selects by max reuse.
+//           Launched with programmatic dependent launch so its prologue overlaps stage 1.
+//  combine  Alg. A.4 outer selection over gathered shard summaries.
+//  merge    Alg. A.3 online binary merge of two summaries, by max reuse.
+#include <cuda_runtime.h>
+
+#include "fs_device.cuh"
+#include "fs_kernels.h"
+#include "fs_sm100.cuh"
+
+namespace fs {
+
+__device__ __forceinline__ fs_summary to_summary(const State& s) {
+  fs_summary o;
+  const bool defined = s.key > kKeyNegInf;
+  o.max_score = defined ? key_to_float(s.key) : -INFINITY;
+  o.idx = defined ? s.idx : -1;
+  o.log_mass = (defined && s.S > 0.0f) ? o.max_score + logf(s.S) : -INFINITY;
+  return o;
+}
+
+__device__ __forceinline__ State from_summary(const fs_summary& m) {
+  State s = state_empty();
+  if (m.idx >= 0 && !(m.max_score == -INFINITY)) {
+    s.key = order_key(m.max_score);
+    s.idx = m.idx;
+    s.S = (m.log_mass > -INFINITY) ? expf(m.log_mass - m.max_score) : 0.0f;
+  }
+  return s;
+}
+
+constexpr int kReduceThreads = 256;
+
+__global__ void __launch_bounds__(kReduceThreads)
+reduce_kernel(const State* __restrict__ part, const int* __restrict__ part_group, int n_slots, int B,
+              int n_groups, int32_t* idx_out, float* score_out, float* logZ_out, fs_summary* groups_out) {
+  extern __shared__ int sg[];
+  __shared__ State red[kReduceThreads];
+  sm100::pdl_wait();                       // stage-1 results are visible past this point
+  const int b = blockIdx.x, tid = threadIdx.x;
+  for (int s = tid; s < n_slots; s += kReduceThreads) sg[s] = part_group[s];
+  __syncthreads();
+  State acc = state_empty();
+  if (n_groups == 1) {
+    for (int s = tid; s < n_slots; s += kReduceThreads)
+      if (sg[s] >= 0) acc = state_merge(acc, part[(size_t)s * B + b]);
+  } else {
+    for (int k = tid; k < n_groups; k += kReduceThreads) {
+      State g = state_empty();
+      for (int s = 0; s < n_slots; ++s)
+        if (sg[s] == k) g = state_merge(g, part[(size_t)s * B + b]);
+      if (groups_out) groups_out[(size_t)b * n_groups + k] = to_summary(g);
+      acc = state_merge(acc, g);
+    }
+  }
+  red[tid] = acc;
+  __syncthreads();
+  for (int w = kReduceThreads / 2; w > 0; w >>= 1) {
+    if (tid < w) red[tid] = state_merge(red[tid], red[tid + w]);
+    __syncthreads();
+  }
+  if (tid == 0) {
+    const fs_summary f = to_summary(red[0]);
+    if (idx_out) idx_out[b] = f.idx;
+    if (score_out) score_out[b] = f.max_score;
+    if (logZ_out) logZ_out[b] = f.log_mass;
+    if (n_groups == 1 && groups_out) groups_out[b] = f;
+  }
+}
+
+__global__ void combine_kernel(const fs_summary* __restrict__ gathered, int n, int B, int32_t* idx_out,
+                               float* score_out, float* logZ_out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  State acc = state_empty();
+  for (int k = 0; k < n; ++k) acc = state_merge(acc, from_summary(gathered[(size_t)k * B + b]));
+  const fs_summary f = to_summary(acc);
+  idx_out[b] = f.idx;
+  if (score_out) score_out[b] = f.max_score;
+  if (logZ_out) logZ_out[b] = f.log_mass;
+}
+
+__global__ void merge_kernel(const fs_summary* a, const fs_summary* b, fs_summary* out, int count) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const State s = state_merge(from_summary(a[i]), from_summary(b[i]));
+  out[i] = to_summary(s);
+}
+
+__global__ void random_bits_kernel(uint64_t seed, uint64_t step, uint32_t tag, const int32_t* b, const int64_t* v,
+                                   uint32_t* r, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t bi = (uint32_t)b[i];
+  const U4 o = philox4x32_10((uint32_t)v[i], bi >> 2, ctr_step_lo(step), ctr_step_hi(step, tag), (uint32_t)seed,
+                             (uint32_t)(seed >> 32));
+  const uint32_t w[4] = {o.x, o.y, o.z, o.w};
+  r[i] = w[bi & 3];
+}
+
+__global__ void gumbel_kernel(const uint32_t* r, float* g, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    g[i] = gumbel32(r[i]);
+}
+
+cudaError_t launch_reduce(const State* part, const int* part_group, int n_slots, int B, int n_groups,
+                          int32_t* idx_out, float* score_out, float* logZ_out, fs_summary* groups_out,
+                          cudaStream_t stream, bool pdl) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(B);
+  cfg.blockDim = dim3(kReduceThreads);
+  cfg.dynamicSmemBytes = (size_t)n_slots * sizeof(int);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  if (cfg.dynamicSmemBytes > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)cfg.dynamicSmemBytes);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaLaunchKernelEx(&cfg, reduce_kernel, part, part_group, n_slots, B, n_groups, idx_out, score_out,
+                            logZ_out, groups_out);
+}
+
+cudaError_t launch_combine(const fs_summary* gathered, int n, int B, int32_t* idx_out, float* score_out,
+                           float* logZ_out, cudaStream_t stream) {
+  combine_kernel<<<(B + 127) / 128, 128, 0, stream>>>(gathered, n, B, idx_out, score_out, logZ_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_merge(const fs_summary* a, const fs_summary* b, fs_summary* out, int count,
+                         cudaStream_t stream) {
+  merge_kernel<<<(count + 127) / 128, 128, 0, stream>>>(a, b, out, count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_random_bits(uint64_t seed, uint64_t step, uint32_t tag, const int32_t* b, const int64_t* v,
+                               uint32_t* r, int64_t n, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  random_bits_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>(seed, step, tag, b, v, r, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gumbel(const uint32_t* r, float* g, int64_t n, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t blocks = (n + 255) / 256;
+  gumbel_kernel<<<(unsigned)(blocks < 65535 * 16 ? blocks : 65535 * 16), 256, 0, stream>>>(r, g, n);
+  return cudaGetLastError();
+}
+
+}  // namespace fs

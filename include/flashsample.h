@@ -85,6 +85,13 @@ void fs_ctx_destroy(fs_ctx* ctx);
 /* Testing / tuning knobs: force the CUDA-core kernel (1) or the tcgen05 kernel (0, default);
  * cap the persistent grid at `max_ctas` (0 = number of SMs). */
 fs_status fs_ctx_set_option(fs_ctx* ctx, const char* name, int64_t value);
+/* Measurement hook (used by bench.py for the roofline figure).  With option "time_stage1" = 1
+ * every call records a CUDA event pair around each stage-1 (fused kernel) launch on the call's
+ * stream (PDL between stage 1 and stage 2 is disabled while timing).  fs_ctx_query(ctx,
+ * "stage1_ms", &out) waits for the recorded events, returns the summed stage-1 milliseconds and
+ * resets the record; "stage1_launches" returns the number of recorded launches (before a
+ * "stage1_ms" query resets it).  Unknown names -> FS_ERR_INVALID. */
+fs_status fs_ctx_query(fs_ctx* ctx, const char* name, double* out);
 
 /* fs_sample -- fused LM-head projection + exact Gumbel-max sampling (Alg. 2).
  *   h [B,D], W [V,D] (dtype), bias/temperature/mask as above (mask_words = ceil(V/32)).

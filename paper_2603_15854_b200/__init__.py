@@ -21,7 +21,7 @@ from . import _lib
 from ._lib import FS_BF16, FS_F32, FlashSampleError
 
 __all__ = ["sample", "sample_grouped", "sample_shard", "combine_summaries", "merge_summaries",
-           "random_bits", "gumbel_from_bits", "Summaries", "context", "set_option",
+           "random_bits", "gumbel_from_bits", "Summaries", "context", "set_option", "query",
            "FlashSampleError", "version", "sample_from_host"]
 
 _ctx = {}
@@ -46,6 +46,12 @@ def context(device: int | torch.device | None = None) -> int:
 
 def set_option(name: str, value: int, device=None) -> None:
     _lib.check(_lib.lib().fs_ctx_set_option(context(device), name.encode(), int(value)), "fs_ctx_set_option")
+
+
+def query(name: str, device=None) -> float:
+    out = ctypes.c_double()
+    _lib.check(_lib.lib().fs_ctx_query(context(device), name.encode(), ctypes.byref(out)), "fs_ctx_query")
+    return out.value
 
 
 def _stream(t: torch.Tensor):

@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/flashsample.h"
 #include "fs_device.cuh"
@@ -41,6 +42,23 @@ struct fs_ctx {
   int max_ctas = 0;
   int pdl = 1;
   int stages_override = 0;
+  int kbps = 0;                    // 0 = default
+  int dbg_no_mma = 0;
+  int l2promo = 3;                 // CUtensorMapL2promotion for W/h maps (3 = 256B)
+  int w_policy = 1;                // 1: W loads evict_first, 0: no cache hint
+  int epi_sleep = 0;               // ns of backoff in epilogue barrier waits (0 = spin)
+  int unit_rows = 0;               // CTA range granularity (0 = default)
+  // tensor-map cache: encoding costs host microseconds per map; W maps are reused across calls
+  struct MapKey { const void* base; int64_t inner, rows; int box, promo; };
+  struct MapEnt { MapKey k; CUtensorMap m; };
+  std::vector<MapEnt> map_cache;
+  // per-(CTA, segment) W descriptors in device memory (fs_fused_tc.cu), cached per layout
+  struct SegKey { const void* W; int64_t D; int V, G, unit, gs, promo; };
+  struct SegEnt { SegKey k; CUtensorMap* dev; int max_seg; };
+  std::vector<SegEnt> seg_cache;
+  int time_stage1 = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;   // created lazily
+  size_t ev_used = 0;
   PFN_encodeTiled encode = nullptr;
 };
 
@@ -59,18 +77,84 @@ fs_status ensure_ws(fs_ctx* ctx, size_t bytes) {
 }
 
 fs_status make_map(fs_ctx* ctx, CUtensorMap* m, const void* base, int64_t inner, int64_t rows, int box_rows) {
+  for (const auto& e : ctx->map_cache)
+    if (e.k.base == base && e.k.inner == inner && e.k.rows == rows && e.k.box == box_rows &&
+        e.k.promo == ctx->l2promo) {
+      *m = e.m;
+      return FS_OK;
+    }
   const cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)rows};
   const cuuint64_t strides[1] = {(cuuint64_t)inner * 2};
   const cuuint32_t box[2] = {64u, (cuuint32_t)box_rows};
   const cuuint32_t estr[2] = {1u, 1u};
   CUresult r = ctx->encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                           (CUtensorMapL2promotion)ctx->l2promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(FS_ERR_INVALID, "cuTensorMapEncodeTiled failed (code " + std::to_string((int)r) + ")");
+  if (ctx->map_cache.size() >= 64) ctx->map_cache.erase(ctx->map_cache.begin());
+  ctx->map_cache.push_back(fs_ctx::MapEnt{fs_ctx::MapKey{base, inner, rows, box_rows, ctx->l2promo}, *m});
   return FS_OK;
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Host copy of the device partition (fs_epilogue.cuh cta_rows) -- must match it exactly.
+void host_cta_rows(int cta, int G, int V, int unit, int& r0, int& r1) {
+  const int64_t U = (V + unit - 1) / unit;
+  r0 = (int)(unit * ((int64_t)cta * U / G));
+  const int64_t e = unit * ((int64_t)(cta + 1) * U / G);
+  r1 = (int)(e < (int64_t)V ? e : (int64_t)V);
+}
+
+fs_status segment_maps(fs_ctx* ctx, const void* W, int64_t D, int V, int G, int unit, int gs,
+                       const CUtensorMap** out, int* max_seg_out) {
+  for (const auto& e : ctx->seg_cache)
+    if (e.k.W == W && e.k.D == D && e.k.V == V && e.k.G == G && e.k.unit == unit && e.k.gs == gs &&
+        e.k.promo == ctx->l2promo) {
+      *out = e.dev;
+      *max_seg_out = e.max_seg;
+      return FS_OK;
+    }
+  int max_seg = 1;
+  for (int c = 0; c < G; ++c) {
+    int r0, r1, n = 0;
+    host_cta_rows(c, G, V, unit, r0, r1);
+    for (int a = r0; a < r1; a = std::min(r1, (a / gs + 1) * gs)) ++n;
+    max_seg = std::max(max_seg, n);
+  }
+  std::vector<CUtensorMap> maps((size_t)G * max_seg);
+  std::memset(maps.data(), 0, maps.size() * sizeof(CUtensorMap));
+  for (int c = 0; c < G; ++c) {
+    int r0, r1, s = 0;
+    host_cta_rows(c, G, V, unit, r0, r1);
+    for (int a = r0; a < r1; ++s) {
+      const int b = std::min(r1, (a / gs + 1) * gs);
+      const cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)(b - a)};
+      const cuuint64_t strides[1] = {(cuuint64_t)D * 2};
+      const cuuint32_t box[2] = {64u, 128u};
+      const cuuint32_t estr[2] = {1u, 1u};
+      CUresult r = ctx->encode(&maps[(size_t)c * max_seg + s], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                               const_cast<char*>(static_cast<const char*>(W)) + (size_t)a * D * 2, dims, strides, box,
+                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               (CUtensorMapL2promotion)ctx->l2promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return fail(FS_ERR_INVALID, "cuTensorMapEncodeTiled (segment) failed");
+      a = b;
+    }
+  }
+  if (ctx->seg_cache.size() >= 16) {
+    cudaFree(ctx->seg_cache.front().dev);
+    ctx->seg_cache.erase(ctx->seg_cache.begin());
+  }
+  CUtensorMap* dev = nullptr;
+  cudaError_t e = cudaMalloc(&dev, maps.size() * sizeof(CUtensorMap));
+  if (e != cudaSuccess) return fail(FS_ERR_OOM, "descriptor cudaMalloc failed");
+  e = cudaMemcpy(dev, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(e, "descriptor upload");
+  ctx->seg_cache.push_back(fs_ctx::SegEnt{fs_ctx::SegKey{W, D, V, G, unit, gs, ctx->l2promo}, dev, max_seg});
+  *out = dev;
+  *max_seg_out = max_seg;
+  return FS_OK;
+}
 
 struct PathArgs {
   fs_dtype dtype;
@@ -97,16 +181,19 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
   if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
   const bool tc = !ctx->force_simt && a.dtype == FS_BF16 && (a.D % 8 == 0) && aligned16(a.h) && aligned16(a.W);
   const size_t esz = a.dtype == FS_BF16 ? 2 : 4;
-  const int U = (a.V + 15) / 16;
+  const int unit = ctx->unit_rows > 0 ? ctx->unit_rows : 16;
+  const int U = (a.V + unit - 1) / unit;
   int G = std::min(ctx->max_ctas > 0 ? ctx->max_ctas : ctx->num_sms, U);
   int max_seg = 1, n_slots;
+  const CUtensorMap* wmaps = nullptr;
   if (tc) {
-    const int64_t rows_max = 16LL * ((U + G - 1) / G);
-    max_seg = (a.group_size >= a.V) ? 1 : (int)((rows_max + a.group_size - 1) / a.group_size + 1);
-    n_slots = G * max_seg;
+    fs_status st0 = segment_maps(ctx, a.W, a.D, a.V, G, unit, std::min(a.group_size, a.V), &wmaps, &max_seg);
+    if (st0 != FS_OK) return st0;
+    n_slots = (a.group_size >= a.V) ? G : G * max_seg * fs::tc_slots_per_segment();
   } else {
     n_slots = (a.V + 127) / 128;
   }
+  const fs::SlotLayout lay{n_slots, tc ? 0 : 1, G, a.V, max_seg, a.group_size, unit};
   const int chunk = 256;
   const int Bc_max = std::min(a.B, chunk);
   const size_t part_bytes = (size_t)n_slots * Bc_max * sizeof(fs::State);
@@ -134,24 +221,50 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
     p.row_offset = r0;
     p.group_size = a.group_size;
     p.max_seg = max_seg;
+    p.unit_rows = unit;
     p.part = part;
     p.part_group = part_group;
+    cudaEvent_t ev_end = nullptr;
+    if (ctx->time_stage1) {
+      if (ctx->ev_used == ctx->ev_pool.size()) {
+        cudaEvent_t e0, e1;
+        if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess)
+          return fail(FS_ERR_CUDA, "cudaEventCreate");
+        ctx->ev_pool.emplace_back(e0, e1);
+      }
+      cudaEventRecord(ctx->ev_pool[ctx->ev_used].first, stream);
+      ev_end = ctx->ev_pool[ctx->ev_used].second;
+      ++ctx->ev_used;
+    }
     if (tc) {
       const int BN = fs::tc_block_n(Bc);
-      p.stages = ctx->stages_override > 0 ? ctx->stages_override : fs::tc_stages(BN);
-      fs::TcMaps maps;
-      if ((st = make_map(ctx, &maps.w128, a.W, a.D, a.V, 128)) != FS_OK) return st;
-      if ((st = make_map(ctx, &maps.w16, a.W, a.D, a.V, 16)) != FS_OK) return st;
-      if ((st = make_map(ctx, &maps.h, p.h, a.D, Bc, BN)) != FS_OK) return st;
-      e = fs::launch_fused_tc(maps, p, BN, a.lse, G, stream);
+      // K slices per TMA stage: as many as keep >= 3 stages in flight (more contiguous bytes per
+      // W row per request -> better DRAM row locality; measured on B200).
+      p.dbg_no_mma = ctx->dbg_no_mma;
+      p.w_policy = ctx->w_policy;
+      p.epi_sleep = ctx->epi_sleep;
+      p.kbps = ctx->kbps;
+      if (p.kbps <= 0) {
+        p.kbps = 1;
+        for (int k = 4; k >= 2; --k)
+          if (fs::tc_stages(BN, k) >= 3) { p.kbps = k; break; }
+      }
+      p.stages = ctx->stages_override > 0 ? ctx->stages_override : fs::tc_stages(BN, p.kbps);
+      if (p.stages < 2) return fail(FS_ERR_INVALID, "K slices per stage too large for shared memory");
+      CUtensorMap hmap;
+      if ((st = make_map(ctx, &hmap, p.h, a.D, Bc, BN)) != FS_OK) return st;
+      p.wmaps = wmaps;
+      e = fs::launch_fused_tc(hmap, p, BN, a.lse, G, stream);
       if (e != cudaSuccess) return cuda_fail(e, "stage-1 tcgen05 kernel launch");
     } else {
       e = fs::launch_fused_simt(p, a.dtype, a.lse, stream);
       if (e != cudaSuccess) return cuda_fail(e, "stage-1 CUDA-core kernel launch");
     }
-    e = fs::launch_reduce(part, part_group, n_slots, Bc, a.n_groups, a.idx_out ? a.idx_out + r0 : nullptr,
+    if (ev_end) cudaEventRecord(ev_end, stream);
+    e = fs::launch_reduce(part, part_group, lay, Bc, a.n_groups, a.idx_out ? a.idx_out + r0 : nullptr,
                           a.score_out ? a.score_out + r0 : nullptr, a.logZ_out ? a.logZ_out + r0 : nullptr,
-                          a.groups_out ? a.groups_out + (size_t)r0 * a.n_groups : nullptr, stream, ctx->pdl != 0);
+                          a.groups_out ? a.groups_out + (size_t)r0 * a.n_groups : nullptr, stream,
+                          ctx->pdl != 0 && !ctx->time_stage1);
     if (e != cudaSuccess) return cuda_fail(e, "stage-2 reduce launch");
   }
   return FS_OK;
@@ -215,6 +328,11 @@ fs_status fs_ctx_create(int device, fs_ctx** out) {
 
 void fs_ctx_destroy(fs_ctx* ctx) {
   if (!ctx) return;
+  for (auto& e : ctx->seg_cache) cudaFree(e.dev);
+  for (auto& pr : ctx->ev_pool) {
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
+  }
   if (ctx->ws) cudaFree(ctx->ws);
   delete ctx;
 }
@@ -225,8 +343,46 @@ fs_status fs_ctx_set_option(fs_ctx* ctx, const char* name, int64_t value) {
   else if (!strcmp(name, "max_ctas")) ctx->max_ctas = (int)value;
   else if (!strcmp(name, "pdl")) ctx->pdl = (int)value;
   else if (!strcmp(name, "stages")) ctx->stages_override = (int)value;
+  else if (!strcmp(name, "kbps")) ctx->kbps = (int)value;
+  else if (!strcmp(name, "dbg_no_mma")) ctx->dbg_no_mma = (int)value;
+  else if (!strcmp(name, "l2promo")) ctx->l2promo = (int)value;
+  else if (!strcmp(name, "w_policy")) ctx->w_policy = (int)value;
+  else if (!strcmp(name, "epi_sleep")) ctx->epi_sleep = (int)value;
+  else if (!strcmp(name, "unit_rows")) {
+    if (value != 0 && value != 16 && value != 32 && value != 64 && value != 128)
+      return fail(FS_ERR_INVALID, "unit_rows must be 0, 16, 32, 64 or 128");
+    ctx->unit_rows = (int)value;
+  }
+  else if (!strcmp(name, "time_stage1")) { ctx->time_stage1 = (int)value; ctx->ev_used = 0; }
   else return fail(FS_ERR_INVALID, std::string("unknown option ") + name);
   return FS_OK;
+}
+
+fs_status fs_ctx_query(fs_ctx* ctx, const char* name, double* out) {
+  if (!ctx || !name || !out) return fail(FS_ERR_INVALID, "ctx, name and out are required");
+  if (!strcmp(name, "stage1_launches")) {
+    *out = (double)ctx->ev_used;
+    return FS_OK;
+  }
+  if (!strcmp(name, "stage1_ms")) {
+    double total = 0.0;
+    for (size_t i = 0; i < ctx->ev_used; ++i) {
+      cudaError_t e = cudaEventSynchronize(ctx->ev_pool[i].second);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaEventSynchronize");
+      float ms = 0.f;
+      e = cudaEventElapsedTime(&ms, ctx->ev_pool[i].first, ctx->ev_pool[i].second);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaEventElapsedTime");
+      total += ms;
+    }
+    ctx->ev_used = 0;
+    *out = total;
+    return FS_OK;
+  }
+  if (!strcmp(name, "num_sms")) {
+    *out = (double)ctx->num_sms;
+    return FS_OK;
+  }
+  return fail(FS_ERR_INVALID, std::string("unknown query ") + name);
 }
 
 fs_status fs_sample(fs_ctx* ctx, fs_dtype dtype, const void* h, const void* W, const float* bias,

@@ -109,13 +109,109 @@ __device__ __forceinline__ void flush_states(State (&st)[NCHUNK], State* scratch
   sm100::named_bar_sync(bar_id, 128);
 }
 
-// Persistent-CTA vocabulary partition: CTA c of G owns rows [16*floor(c*U/G), 16*floor((c+1)*U/G))
-// (U = ceil(V/16) 16-row units), clipped to V.  Balanced to one 16-row unit, so no CTA streams
-// more than ceil(U/G)*16 rows of W (no split-K, so every logit's fp32 sum is independent of G).
-__device__ __forceinline__ void cta_rows(int cta, int G, int V, int& r0, int& r1) {
-  const int64_t U = (V + 15) / 16;
-  r0 = (int)(16 * ((int64_t)cta * U / G));
-  const int64_t e = 16 * ((int64_t)(cta + 1) * U / G);
+// ---------------------------------------------------------------------------------------------
+// tcgen05 epilogue: one warp processes its 32 TMEM lanes (vocabulary rows) x all B columns of one
+// accumulator tile, in rolled groups of 8 columns.  Per group: issue the TMEM load, generate the
+// 8 Philox/Gumbel draws (independent of the accumulator, so they overlap the load), wait, then
+// transform + key + warp argmax for the 8 columns back to back (independent chains).
+// Running states: st[c] holds this lane's state for column 32c + lane; chunk c is processed at
+// st[0] and the array is rotated, so the loops stay rolled (small code, no local memory).
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ void rotate_states(State (&st)[8]) {
+  const State t = st[0];
+#pragma unroll
+  for (int i = 0; i < 7; ++i) st[i] = st[i + 1];
+  st[7] = t;
+}
+
+template <bool LSE, bool XFORM>
+__device__ __forceinline__ void epi_tile_tc(uint32_t taddr, const RowArgs& ra, const EpiArgs& ea, State (&st)[8],
+                                            int lane, uint64_t* tempty) {
+  const int B = ea.B;
+  const int nch = (B + 31) >> 5;
+#pragma unroll 1
+  for (int c = 0; c < nch; ++c) {
+    State own = st[0];
+#pragma unroll 1
+    for (int g = 0; g < 4; ++g) {
+      const int col0 = c * 32 + g * 8;
+      if (col0 >= B) break;
+      uint32_t r[8];
+      sm100::tmem_ld_32x32b_x8(taddr + (uint32_t)col0, r);
+      const uint32_t qd = (uint32_t)(ea.row_offset + col0) >> 2;
+      const U4 p0 = philox4x32_10(ra.v_lo, qd, ea.c2, ea.c3, ea.k0, ea.k1);
+      const U4 p1 = philox4x32_10(ra.v_lo, qd + 1u, ea.c2, ea.c3, ea.k0, ea.k1);
+      const float gm[8] = {gumbel32(p0.x), gumbel32(p0.y), gumbel32(p0.z), gumbel32(p0.w),
+                           gumbel32(p1.x), gumbel32(p1.y), gumbel32(p1.z), gumbel32(p1.w)};
+      sm100::tmem_wait_ld();
+      if (col0 + 8 >= B) {                      // last TMEM read of this tile: free the buffer
+        sm100::tc_fence_before();
+        sm100::mbar_arrive(tempty);
+      }
+      uint32_t key[8];
+      float lt[8];
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        float l = __uint_as_float(r[jj]);
+        if (XFORM) {
+          l = (l + ra.bias) * ea.invtau[col0 + jj];
+          if (ea.mask != nullptr && col0 + jj < B) {
+            const uint32_t w = __ldg(ea.mask + (int64_t)(col0 + jj) * ea.mask_words + (ra.v_global >> 5));
+            if (!((w >> (ra.v_global & 31)) & 1u)) l = -INFINITY;
+          }
+        }
+        if (isnan(l)) l = -INFINITY;
+        lt[jj] = l;
+        key[jj] = ra.valid ? order_key(l + gm[jj]) : kKeyNone;
+      }
+      uint32_t kmax[8], ball[8];
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) kmax[jj] = __reduce_max_sync(0xFFFFFFFFu, key[jj]);
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) ball[jj] = __ballot_sync(0xFFFFFFFFu, key[jj] == kmax[jj]);
+      float Sw[8];
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        Sw[jj] = 0.0f;
+        if (LSE) {
+          const float m = key_ref(kmax[jj]);
+          float e = (ra.valid && m != -INFINITY) ? fast_exp2((lt[jj] - m) * kLog2e) : 0.0f;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xFFFFFFFFu, e, o);
+          Sw[jj] = e;
+        }
+      }
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj)
+        if (lane == g * 8 + jj)
+          absorb<LSE>(own, kmax[jj], kmax[jj] > kKeyNone ? ra.warp_v0 + (__ffs(ball[jj]) - 1) : -1, Sw[jj]);
+    }
+    st[0] = own;
+    if (nch > 1) rotate_states(st);
+  }
+  if (nch > 1)
+#pragma unroll 1
+    for (int i = nch; i < 8; ++i) rotate_states(st);       // restore chunk order
+}
+
+// Write this warp's states (one candidate per column for its 32 rows of every tile it saw in
+// the segment) to its own candidate slot; stage 2 merges slots (no intra-CTA barrier needed).
+__device__ __forceinline__ void flush_warp(State (&st)[8], int lane, int B, State* part_row) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int b = c * 32 + lane;
+    if (b < B) part_row[b] = st[c];
+    st[c] = state_empty();
+  }
+}
+
+// Persistent-CTA vocabulary partition: CTA c of G owns rows [u*floor(c*U/G), u*floor((c+1)*U/G))
+// (U = ceil(V/u) units of u rows, u in {16, 32, 64, 128}), clipped to V.  No split-K: every
+// logit's fp32 sum is independent of G and of the partition.
+__device__ __forceinline__ void cta_rows(int cta, int G, int V, int unit, int& r0, int& r1) {
+  const int64_t U = (V + unit - 1) / unit;
+  r0 = (int)(unit * ((int64_t)cta * U / G));
+  const int64_t e = unit * ((int64_t)(cta + 1) * U / G);
   r1 = (int)(e < (int64_t)V ? e : (int64_t)V);
 }
 // Tiles are the intersections of the CTA's rows with 128-aligned blocks, so a tile never

@@ -4,15 +4,20 @@
 // whose epilogue samples instead of storing logits:
 //   * grid = #SMs persistent CTAs, each owning a balanced contiguous range of vocabulary rows
 //     (16-row granularity, fs_epilogue.cuh cta_rows): W is streamed from HBM exactly once.
+//     The range is cut at group boundaries into segments; each segment has its own TMA
+//     descriptor whose row extent is the segment itself, so every W load is one full 128-row
+//     box and the ragged last tile is clipped by TMA out-of-bounds handling (no DRAM traffic,
+//     no small boxes -- small boxes cost ~12% of stream bandwidth on B200).
 //   * MMA shape M = 128 vocabulary rows (A = W tile, K-major) x N = BN batch rows (B = h tile,
 //     K-major, zero-filled past B by TMA) x K = 16, fp32 accumulation in TMEM.
 //   * warp 0: TMA producer (W with L2 evict_first, h with evict_last) into an S-stage ring of
-//             64-wide K slices (128-byte swizzle);
-//     warp 1: TMEM allocator + single-thread MMA issuer; double-buffered accumulators (2 x BN
-//             columns) so the epilogue of tile t overlaps the MMAs of tile t+1;
-//     warps 2-5: epilogue, one per TMEM lane quadrant: tcgen05.ld -> registers -> transform +
-//             Philox + Gumbel + warp argmax (fs_epilogue.cuh) -> one candidate per (row, CTA,
-//             group segment) written to the candidate buffer.  Logits never leave the SM.
+//             KBPS 64-wide K slices per stage (128-byte swizzle);
+//     warp 1: TMEM allocator + single-thread MMA issuer; two accumulator buffers (2 x BN TMEM
+//             columns), tile t goes to buffer t mod 2;
+//     warps 2-9: two epilogue warpgroups; group s drains buffer s (tiles s, s+2, ...), one warp
+//             per TMEM lane quadrant: tcgen05.ld -> registers -> transform + Philox + Gumbel +
+//             warp argmax (fs_epilogue.cuh) -> candidates.  Logits never leave the SM; the
+//             only HBM writes are the candidates.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -21,46 +26,44 @@
 
 namespace fs {
 
-constexpr int kThreadsTC = 192;          // 6 warps
+constexpr int kEpiWarps = 8;
+constexpr int kThreadsTC = 64 + 32 * kEpiWarps;   // 10 warps
 constexpr int kBlockM = 128;
-constexpr int kBlockK = 64;              // 64 bf16 = 128 B = one swizzle row
+constexpr int kBlockK = 64;                       // 64 bf16 = 128 B = one swizzle row
 constexpr int kWStageBytes = kBlockM * kBlockK * 2;
+constexpr int kExtraBytes = 64 * 8 + 16 + 256 * 4 + 64;   // barriers, tmem slot, invtau[256]
 
-template <int BN>
-struct TcCfg {
-  static constexpr int kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
-                                   : (2 * BN <= 256) ? 256 : 512;
-  static constexpr int kHStageBytes = BN * kBlockK * 2;
-  static constexpr int kStageBytes = kWStageBytes + kHStageBytes;
-  static constexpr int kColsPerChunk = BN < 32 ? BN : 32;
-  static constexpr int kChunks = BN / kColsPerChunk;
-  // bytes after the stage ring: 2S+4 mbarriers, tmem address, invtau[BN], scratch[4][BN]
-  static constexpr int extra_bytes(int S) { return (2 * S + 4) * 8 + 16 + BN * 4 + 4 * BN * 16 + 64; }
-};
+static int tmem_cols_for(int BN) {
+  int c = 32;
+  while (c < 2 * BN) c <<= 1;
+  return c;
+}
 
-template <int BN, bool LSE>
+// Segments of a CTA range: [a, b) = intersection of [r0, r1) with one group; tiles are
+// [a + 128k, min(b, a + 128(k+1))).
+__device__ __forceinline__ int seg_end(int a, int r1, int gs) { return min(r1, (a / gs + 1) * gs); }
+
+template <bool LSE, bool XFORM>
 __global__ void __launch_bounds__(kThreadsTC, 1)
-fused_tc_kernel(const __grid_constant__ CUtensorMap tmW128, const __grid_constant__ CUtensorMap tmW16,
-                const __grid_constant__ CUtensorMap tmH, const StageOneParams p) {
-  using Cfg = TcCfg<BN>;
+fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int S = p.stages;
+  const int S = p.stages, BN = p.bn, KBPS = p.kbps;
+  const int h_stage_bytes = BN * kBlockK * 2;                 // per 64-wide K slice
   uint8_t* w_ring = smem;
-  uint8_t* h_ring = smem + (size_t)S * kWStageBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(h_ring + (size_t)S * Cfg::kHStageBytes);
+  uint8_t* h_ring = smem + (size_t)S * KBPS * kWStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(h_ring + (size_t)S * KBPS * h_stage_bytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* invtau = reinterpret_cast<float*>(tmem_slot + 4);
-  State* scratch = reinterpret_cast<State*>(invtau + BN);
+  const CUtensorMap* wmaps = p.wmaps + (size_t)blockIdx.x * p.max_seg;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    sm100::prefetch_tmap(&tmW128);
-    sm100::prefetch_tmap(&tmW16);
     sm100::prefetch_tmap(&tmH);
+    for (int s = 0; s < p.max_seg; ++s) sm100::prefetch_tmap(&wmaps[s]);
     for (int s = 0; s < S; ++s) {
       sm100::mbar_init(&full[s], 1);
       sm100::mbar_init(&empty[s], 1);
@@ -71,14 +74,16 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmW128, const __grid_constan
     }
     sm100::fence_barrier_init();
   }
-  if (warp == 1) sm100::tmem_alloc<Cfg::kTmemCols>(tmem_slot);
-  for (int b = threadIdx.x; b < BN; b += kThreadsTC) {
-    float it = __int_as_float(0x7FC00000);                 // NaN: padding column / invalid tau
-    if (b < p.B) {
-      const float t = p.temperature ? p.temperature[b] : 1.0f;
-      if (t > 0.0f && isfinite(t)) it = 1.0f / t;
+  if (warp == 1) sm100::tmem_alloc(tmem_slot, (uint32_t)p.tmem_cols);
+  if (XFORM) {
+    for (int b = threadIdx.x; b < 256; b += kThreadsTC) {
+      float it = __int_as_float(0x7FC00000);               // NaN: padding column / invalid tau
+      if (b < p.B) {
+        const float t = p.temperature ? p.temperature[b] : 1.0f;
+        if (t > 0.0f && isfinite(t)) it = 1.0f / t;
+      }
+      invtau[b] = it;
     }
-    invtau[b] = it;
   }
   sm100::tc_fence_before();
   __syncthreads();
@@ -87,71 +92,81 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmW128, const __grid_constan
   sm100::pdl_launch_dependents();
 
   int r0, r1;
-  cta_rows(blockIdx.x, gridDim.x, p.V, r0, r1);
+  cta_rows(blockIdx.x, gridDim.x, p.V, p.unit_rows, r0, r1);
   const int num_kb = (p.D + kBlockK - 1) / kBlockK;
+  const int gs = p.group_size;
 
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------ TMA producer ------------------------------------
-      const uint64_t pol_w = sm100::policy_evict_first(), pol_h = sm100::policy_evict_last();
+      const uint64_t pol_w = p.w_policy ? sm100::policy_evict_first() : sm100::policy_evict_normal();
+      const uint64_t pol_h = sm100::policy_evict_last();
+      const uint32_t stage_tx = (uint32_t)(kWStageBytes + h_stage_bytes);   // full boxes, OOB counted
       int stage = 0;
       uint32_t phase = 0;
-      for (int t0 = r0; t0 < r1;) {
-        const int t1 = tile_end(t0, r1), base = t0 & ~127;
-        const bool full_tile = (t0 == base) && (t1 - t0 == kBlockM);
-        const int nbox = (t1 - t0 + 15) >> 4;
-        const uint32_t bytes = (full_tile ? kWStageBytes : nbox * 16 * kBlockK * 2) + Cfg::kHStageBytes;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          sm100::mbar_wait(&empty[stage], phase ^ 1);
-          sm100::mbar_arrive_expect_tx(&full[stage], bytes);
-          uint8_t* wdst = w_ring + (size_t)stage * kWStageBytes;
-          if (full_tile) {
-            sm100::tma_load_2d(wdst, &tmW128, &full[stage], kb * kBlockK, t0, pol_w);
-          } else {
-            for (int j = 0; j < nbox; ++j)
-              sm100::tma_load_2d(wdst + (t0 - base + 16 * j) * (kBlockK * 2), &tmW16, &full[stage], kb * kBlockK,
-                                 t0 + 16 * j, pol_w);
+      int seg = 0;
+      for (int a = r0; a < r1; ++seg) {
+        const int b = seg_end(a, r1, gs);
+        const CUtensorMap* wm = &wmaps[seg];
+        for (int t0 = a; t0 < b; t0 += kBlockM) {
+          for (int kb0 = 0; kb0 < num_kb; kb0 += KBPS) {
+            const int nk = min(KBPS, num_kb - kb0);
+            sm100::mbar_wait(&empty[stage], phase ^ 1);
+            sm100::mbar_arrive_expect_tx(&full[stage], stage_tx * nk);
+            for (int j = 0; j < nk; ++j) {
+              const int kb = kb0 + j;
+              sm100::tma_load_2d(w_ring + ((size_t)stage * KBPS + j) * kWStageBytes, wm, &full[stage],
+                                 kb * kBlockK, t0 - a, pol_w);
+              sm100::tma_load_2d(h_ring + ((size_t)stage * KBPS + j) * h_stage_bytes, &tmH, &full[stage],
+                                 kb * kBlockK, 0, pol_h);
+            }
+            if (++stage == S) { stage = 0; phase ^= 1; }
           }
-          sm100::tma_load_2d(h_ring + (size_t)stage * Cfg::kHStageBytes, &tmH, &full[stage], kb * kBlockK, 0,
-                             pol_h);
-          if (++stage == S) { stage = 0; phase ^= 1; }
         }
-        t0 = t1;
+        a = b;
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       // ------------------------------ MMA issuer --------------------------------------
-      constexpr uint32_t idesc = sm100::umma_idesc_bf16(kBlockM, BN);
+      const uint32_t idesc = sm100::umma_idesc_bf16(kBlockM, BN);
       int stage = 0;
       uint32_t phase = 0;
       int tile_i = 0;
-      for (int t0 = r0; t0 < r1; ++tile_i) {
-        const int t1 = tile_end(t0, r1);
-        const int buf = tile_i & 1;
-        const uint32_t use = (uint32_t)(tile_i >> 1);
-        sm100::mbar_wait(&tempty[buf], (use & 1) ^ 1);
-        sm100::tc_fence_after();
-        const uint32_t d_tmem = tmem_base + (uint32_t)(buf * BN);
-        for (int kb = 0; kb < num_kb; ++kb) {
-          sm100::mbar_wait(&full[stage], phase);
+      for (int a = r0; a < r1;) {
+        const int b = seg_end(a, r1, gs);
+        for (int t0 = a; t0 < b; t0 += kBlockM, ++tile_i) {
+          const int buf = tile_i & 1;
+          const uint32_t use = (uint32_t)(tile_i >> 1);
+          sm100::mbar_wait(&tempty[buf], (use & 1) ^ 1);
           sm100::tc_fence_after();
-          const uint64_t adesc = sm100::umma_desc_sw128(sm100::smem_u32(w_ring + (size_t)stage * kWStageBytes));
-          const uint64_t bdesc = sm100::umma_desc_sw128(sm100::smem_u32(h_ring + (size_t)stage * Cfg::kHStageBytes));
+          const uint32_t d_tmem = tmem_base + (uint32_t)(buf * BN);
+          for (int kb0 = 0; kb0 < num_kb; kb0 += KBPS) {
+            const int nk = p.dbg_no_mma ? 0 : min(KBPS, num_kb - kb0);
+            sm100::mbar_wait(&full[stage], phase);
+            sm100::tc_fence_after();
+            for (int j = 0; j < nk; ++j) {
+              const uint64_t adesc =
+                  sm100::umma_desc_sw128(sm100::smem_u32(w_ring + ((size_t)stage * KBPS + j) * kWStageBytes));
+              const uint64_t bdesc =
+                  sm100::umma_desc_sw128(sm100::smem_u32(h_ring + ((size_t)stage * KBPS + j) * h_stage_bytes));
 #pragma unroll
-          for (int k = 0; k < kBlockK / 16; ++k)
-            sm100::mma_bf16_ss(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
-          sm100::mma_commit(&empty[stage]);
-          if (++stage == S) { stage = 0; phase ^= 1; }
+              for (int k = 0; k < kBlockK / 16; ++k)
+                sm100::mma_bf16_ss(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, ((kb0 + j) | k) != 0 ? 1u : 0u);
+            }
+            sm100::mma_commit(&empty[stage]);
+            if (++stage == S) { stage = 0; phase ^= 1; }
+          }
+          sm100::mma_commit(&tfull[buf]);
         }
-        sm100::mma_commit(&tfull[buf]);
-        t0 = t1;
+        a = b;
       }
     }
   } else {
     // -------------------------------- epilogue ------------------------------------------
+    const int e = warp - 2;                       // 0..7
+    const int set = e >> 2;                       // drains TMEM buffer `set`
     const int q = warp & 3;                       // TMEM lane quadrant this warp may access
-    const int epi_tid = threadIdx.x - 64;
     EpiArgs ea;
     ea.invtau = invtau;
     ea.mask = p.mask;
@@ -162,78 +177,69 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmW128, const __grid_constan
     ea.k1 = (uint32_t)(p.seed >> 32);
     ea.c2 = ctr_step_lo(p.step);
     ea.c3 = ctr_step_hi(p.step, 0u);
-    State st[Cfg::kChunks];
+    State st[8];
 #pragma unroll
-    for (int c = 0; c < Cfg::kChunks; ++c) st[c] = state_empty();
-    int seg = 0, cur_group = -1, tile_i = 0;
-    State* part_cta = p.part + (size_t)blockIdx.x * p.max_seg * p.B;
-    for (int t0 = r0; t0 < r1; ++tile_i) {
-      const int t1 = tile_end(t0, r1), base = t0 & ~127;
-      const int grp = t0 / p.group_size;
-      if (cur_group >= 0 && grp != cur_group) {
-        flush_states<Cfg::kChunks, Cfg::kColsPerChunk>(st, scratch, BN, q, lane, epi_tid, p.B,
-                                                      part_cta + (size_t)seg * p.B, 1);
-        if (epi_tid == 0) p.part_group[blockIdx.x * p.max_seg + seg] = cur_group;
-        ++seg;
+    for (int c = 0; c < 8; ++c) st[c] = state_empty();
+    const int slot0 = blockIdx.x * p.max_seg;
+    int tile_i = 0, seg = 0;
+    for (int a = r0; a < r1; ++seg) {
+      const int b = seg_end(a, r1, gs);
+      for (int t0 = a; t0 < b; t0 += kBlockM, ++tile_i) {
+        if ((tile_i & 1) != set) continue;
+        const int t1 = min(b, t0 + kBlockM);
+        const uint32_t use = (uint32_t)(tile_i >> 1);
+        if (p.epi_sleep) sm100::mbar_wait_sleep(&tfull[set], use & 1, (uint32_t)p.epi_sleep);
+        else sm100::mbar_wait(&tfull[set], use & 1);
+        sm100::tc_fence_after();
+        const int row = t0 + 32 * q + lane;     // TMEM lane l of this tile = row t0 + l
+        RowArgs ra;
+        ra.valid = row < t1;
+        ra.v_global = (int32_t)(p.vocab_offset + row);
+        ra.v_lo = (uint32_t)ra.v_global;
+        ra.warp_v0 = (int32_t)(p.vocab_offset + t0 + 32 * q);
+        ra.bias = (XFORM && ra.valid && p.bias) ? p.bias[row] : 0.0f;
+        const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(set * BN);
+        epi_tile_tc<LSE, XFORM>(taddr, ra, ea, st, lane, &tempty[set]);
       }
-      cur_group = grp;
-      const int buf = tile_i & 1;
-      const uint32_t use = (uint32_t)(tile_i >> 1);
-      sm100::mbar_wait(&tfull[buf], use & 1);
-      sm100::tc_fence_after();
-      const int row = base + 32 * q + lane;
-      RowArgs ra;
-      ra.valid = row >= t0 && row < t1;
-      ra.v_global = (int32_t)(p.vocab_offset + row);
-      ra.v_lo = (uint32_t)ra.v_global;
-      ra.warp_v0 = (int32_t)(p.vocab_offset + base + 32 * q);
-      ra.bias = (ra.valid && p.bias) ? p.bias[row] : 0.0f;
-      const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * BN);
-#pragma unroll
-      for (int c = 0; c < Cfg::kChunks; ++c) {
-        uint32_t r[32];
-        if constexpr (Cfg::kColsPerChunk == 32) sm100::tmem_ld_32x32b_x32(taddr + c * 32, r);
-        else sm100::tmem_ld_32x32b_x16(taddr, r);
-        sm100::tmem_wait_ld();
-        if (c == Cfg::kChunks - 1) {
-          sm100::tc_fence_before();
-          sm100::mbar_arrive(&tempty[buf]);        // accumulator buffer free for tile t+2
-        }
-        float acc[32];
-#pragma unroll
-        for (int i = 0; i < Cfg::kColsPerChunk; ++i) acc[i] = __uint_as_float(r[i]);
-        epi_columns<Cfg::kColsPerChunk, LSE>(acc, c * Cfg::kColsPerChunk, ra, ea, st[c], lane);
+      if (gs < p.V) {                           // grouped: one candidate slot per (segment, warp)
+        const int slot = (slot0 + seg) * kEpiWarps + e;
+        flush_warp(st, lane, p.B, p.part + (size_t)slot * p.B);
+        if (lane == 0) p.part_group[slot] = a / gs;
       }
-      t0 = t1;
+      a = b;
     }
-    if (cur_group >= 0) {
-      flush_states<Cfg::kChunks, Cfg::kColsPerChunk>(st, scratch, BN, q, lane, epi_tid, p.B,
-                                                    part_cta + (size_t)seg * p.B, 1);
-      if (epi_tid == 0) p.part_group[blockIdx.x * p.max_seg + seg] = cur_group;
-      ++seg;
+    if (gs < p.V) {
+      if (lane == 0)
+        for (int s = seg; s < p.max_seg; ++s) p.part_group[(slot0 + s) * kEpiWarps + e] = -1;
+    } else {
+      // Single group: all tiles are drained, so every MMA has consumed its stage and the TMA
+      // ring is free; use it as scratch to merge the 8 warps' candidates into ONE slot per CTA
+      // (stage 2 then reads #CTA candidates per row instead of 8 x #CTA).
+      sm100::named_bar_sync(1, 32 * kEpiWarps);
+      State* scratch = reinterpret_cast<State*>(w_ring);        // [8][BN] <= 32 KB
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int bb = c * 32 + lane;
+        if (bb < BN) scratch[e * BN + bb] = st[c];
+      }
+      sm100::named_bar_sync(1, 32 * kEpiWarps);
+      const int et = threadIdx.x - 64;                          // 0..255
+      for (int bb = et; bb < p.B; bb += 32 * kEpiWarps) {
+        State m = scratch[bb];
+#pragma unroll
+        for (int w = 1; w < kEpiWarps; ++w) m = state_merge(m, scratch[w * BN + bb]);
+        p.part[(size_t)blockIdx.x * p.B + bb] = m;              // compact: slot = CTA
+      }
+      if (et == 0) p.part_group[blockIdx.x] = (r0 < r1) ? 0 : -1;
     }
-    if (epi_tid == 0)
-      for (int s = seg; s < p.max_seg; ++s) p.part_group[blockIdx.x * p.max_seg + s] = -1;
   }
 
   sm100::tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     sm100::tc_fence_after();
-    sm100::tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+    sm100::tmem_dealloc(tmem_base, (uint32_t)p.tmem_cols);
   }
-}
-
-template <int BN, bool LSE>
-static cudaError_t launch_bn(const TcMaps& maps, const StageOneParams& p, int grid, cudaStream_t stream) {
-  using Cfg = TcCfg<BN>;
-  const int S = p.stages;
-  const size_t smem = 1024 + (size_t)S * Cfg::kStageBytes + Cfg::extra_bytes(S);
-  auto kern = fused_tc_kernel<BN, LSE>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  kern<<<grid, kThreadsTC, smem, stream>>>(maps.w128, maps.w16, maps.h, p);
-  return cudaGetLastError();
 }
 
 int tc_block_n(int B) {
@@ -242,33 +248,34 @@ int tc_block_n(int B) {
   return ((B + 31) / 32) * 32;
 }
 
-int tc_stages(int BN) {
+int tc_stages(int BN, int kbps) {
   const int budget = 227 * 1024 - 1024;
-  const int stage = kWStageBytes + BN * kBlockK * 2;
+  const int stage = (kWStageBytes + BN * kBlockK * 2) * kbps;
   int S = 16;
-  while (S > 2 && S * stage + ((2 * S + 4) * 8 + 16 + BN * 4 + 4 * BN * 16 + 64) > budget) --S;
+  while (S > 0 && S * stage + kExtraBytes > budget) --S;
   return S;
 }
 
-cudaError_t launch_fused_tc(const TcMaps& maps, const StageOneParams& p, int BN, bool lse, int grid,
+int tc_slots_per_segment() { return kEpiWarps; }
+
+cudaError_t launch_fused_tc(const CUtensorMap& hmap, const StageOneParams& p_in, int BN, bool lse, int grid,
                             cudaStream_t stream) {
-#define FS_CASE(N)                                                                     \
-  case N:                                                                              \
-    return lse ? launch_bn<N, true>(maps, p, grid, stream) : launch_bn<N, false>(maps, p, grid, stream);
-  switch (BN) {
-    FS_CASE(16)
-    FS_CASE(32)
-    FS_CASE(64)
-    FS_CASE(96)
-    FS_CASE(128)
-    FS_CASE(160)
-    FS_CASE(192)
-    FS_CASE(224)
-    FS_CASE(256)
-    default:
-      return cudaErrorInvalidValue;
+  StageOneParams p = p_in;
+  p.bn = BN;
+  p.tmem_cols = tmem_cols_for(BN);
+  const size_t smem = 1024 + (size_t)p.stages * p.kbps * (kWStageBytes + BN * kBlockK * 2) + kExtraBytes;
+  const bool xform = p.bias || p.temperature || p.mask;
+  auto kern = lse ? (xform ? fused_tc_kernel<true, true> : fused_tc_kernel<true, false>)
+                  : (xform ? fused_tc_kernel<false, true> : fused_tc_kernel<false, false>);
+  static bool attr_set[4] = {false, false, false, false};
+  const int variant = (lse ? 2 : 0) + (xform ? 1 : 0);
+  if (!attr_set[variant]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_set[variant] = true;
   }
-#undef FS_CASE
+  kern<<<grid, kThreadsTC, smem, stream>>>(hmap, p);
+  return cudaGetLastError();
 }
 
 }  // namespace fs

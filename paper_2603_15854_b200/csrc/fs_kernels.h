@@ -25,23 +25,40 @@ struct StageOneParams {
   int group_size;             // local rows per group (multiple of 128); >= V for one group
   int max_seg;                // candidate slots per CTA
   int stages;                 // TMA ring depth (TC kernel)
+  int unit_rows;              // CTA range granularity in rows (TC kernel): 16, 32, 64 or 128
+  int kbps;                   // 64-wide K slices per ring stage (TC kernel)
+  int dbg_no_mma;             // debug: stream operands through the ring without issuing MMAs
+  int w_policy;               // 1: W TMA loads carry an L2 evict_first hint
+  int epi_sleep;              // ns backoff while epilogue warps wait for an accumulator
+  int bn;                     // MMA N (batch columns, padded) (TC kernel; set by launch_fused_tc)
+  int tmem_cols;              // TMEM columns allocated (TC kernel; set by launch_fused_tc)
+  const CUtensorMap* wmaps;   // [grid][max_seg] device TMA descriptors of each CTA segment (TC kernel)
   State* part;                // [grid * max_seg][B] candidate states
   int* part_group;            // [grid * max_seg] group id of each slot, -1 = unused
 };
 
-struct TcMaps {
-  CUtensorMap w128, w16, h;
-};
 
 int tc_block_n(int B);
-int tc_stages(int BN);
-cudaError_t launch_fused_tc(const TcMaps& maps, const StageOneParams& p, int BN, bool lse, int grid,
+int tc_stages(int BN, int kbps);
+int tc_slots_per_segment();   // candidate slots one CTA writes per group segment
+cudaError_t launch_fused_tc(const CUtensorMap& hmap, const StageOneParams& p, int BN, bool lse, int grid,
                             cudaStream_t stream);
 // CUDA-core stage 1: grid = ceil(V/128) aligned tiles, one slot per tile.
 cudaError_t launch_fused_simt(const StageOneParams& p, fs_dtype dtype, bool lse, cudaStream_t stream);
 
+// Where stage 1 put the candidates of each group (stage 2 needs it to find a group's slots).
+struct SlotLayout {
+  int n_slots;       // candidate slots written
+  int simt;          // 1: CUDA-core layout, slot = 128-row tile; 0: tcgen05 layout
+  int G;             // tcgen05: persistent CTAs (cta_rows partition)
+  int V;             // local rows
+  int max_seg;       // tcgen05 grouped: segments per CTA (slot = (cta*max_seg + seg)*8 + warp)
+  int group_size;
+  int unit_rows;     // tcgen05: CTA range granularity
+};
+
 // Stage 2: reduce the candidate slots of every row into groups and the final sample.
-cudaError_t launch_reduce(const State* part, const int* part_group, int n_slots, int B, int n_groups,
+cudaError_t launch_reduce(const State* part, const int* part_group, const SlotLayout& lay, int B, int n_groups,
                           int32_t* idx_out, float* score_out, float* logZ_out, fs_summary* groups_out,
                           cudaStream_t stream, bool pdl);
 cudaError_t launch_combine(const fs_summary* gathered, int n, int B, int32_t* idx_out, float* score_out,

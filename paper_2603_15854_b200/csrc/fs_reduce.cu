@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include "fs_device.cuh"
+#include "fs_epilogue.cuh"
 #include "fs_kernels.h"
 #include "fs_sm100.cuh"
 
@@ -35,27 +36,81 @@ __device__ __forceinline__ State from_summary(const fs_summary& m) {
 
 constexpr int kReduceThreads = 256;
 
-__global__ void __launch_bounds__(kReduceThreads)
-reduce_kernel(const State* __restrict__ part, const int* __restrict__ part_group, int n_slots, int B,
-              int n_groups, int32_t* idx_out, float* score_out, float* logZ_out, fs_summary* groups_out) {
-  extern __shared__ int sg[];
-  __shared__ State red[kReduceThreads];
+// Single group (Alg. 2 stage 2; or one TP shard's summary): one warp per batch row,
+// each lane merges slots lane, lane+32, ... (independent loads in flight), then a fixed
+// shuffle tree -- deterministic, so logZ is bit-reproducible.
+__global__ void __launch_bounds__(128)
+reduce_rows_kernel(const State* __restrict__ part, const int* __restrict__ part_group, int n_slots, int B,
+                   int32_t* idx_out, float* score_out, float* logZ_out, fs_summary* groups_out) {
   sm100::pdl_wait();                       // stage-1 results are visible past this point
-  const int b = blockIdx.x, tid = threadIdx.x;
-  for (int s = tid; s < n_slots; s += kReduceThreads) sg[s] = part_group[s];
-  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (b >= B) return;
   State acc = state_empty();
-  if (n_groups == 1) {
-    for (int s = tid; s < n_slots; s += kReduceThreads)
-      if (sg[s] >= 0) acc = state_merge(acc, part[(size_t)s * B + b]);
-  } else {
-    for (int k = tid; k < n_groups; k += kReduceThreads) {
-      State g = state_empty();
-      for (int s = 0; s < n_slots; ++s)
-        if (sg[s] == k) g = state_merge(g, part[(size_t)s * B + b]);
-      if (groups_out) groups_out[(size_t)b * n_groups + k] = to_summary(g);
-      acc = state_merge(acc, g);
-    }
+#pragma unroll 4
+  for (int s = lane; s < n_slots; s += 32)
+    if (part_group[s] >= 0) acc = state_merge(acc, part[(size_t)s * B + b]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    State other;
+    other.key = __shfl_xor_sync(0xFFFFFFFFu, acc.key, o);
+    other.idx = __shfl_xor_sync(0xFFFFFFFFu, acc.idx, o);
+    other.S = __shfl_xor_sync(0xFFFFFFFFu, acc.S, o);
+    other.pad = 0u;
+    acc = (lane & o) ? state_merge(other, acc) : state_merge(acc, other);
+  }
+  if (lane == 0) {
+    const fs_summary f = to_summary(acc);
+    if (idx_out) idx_out[b] = f.idx;
+    if (score_out) score_out[b] = f.max_score;
+    if (logZ_out) logZ_out[b] = f.log_mass;
+    if (groups_out) groups_out[b] = f;
+  }
+}
+
+// Candidate slots of group k: the CTAs whose rows intersect [k g, (k+1) g) (binary search on
+// the persistent partition), each with max_seg x 8 slots tagged by group id.
+__device__ __forceinline__ State merge_group(const State* __restrict__ part, const int* __restrict__ part_group,
+                                             const SlotLayout& L, int B, int b, int k) {
+  State acc = state_empty();
+  const int a = k * L.group_size;
+  const int e = min(L.V, a + L.group_size);
+  if (L.simt) {
+    for (int t = a / 128; t < (e + 127) / 128; ++t) acc = state_merge(acc, part[(size_t)t * B + b]);
+    return acc;
+  }
+  // first CTA with r1 > a, last CTA with r0 < e
+  int lo = 0, hi = L.G - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    int r0, r1;
+    cta_rows(mid, L.G, L.V, L.unit_rows, r0, r1);
+    if (r1 > a) hi = mid; else lo = mid + 1;
+  }
+  for (int c = lo; c < L.G; ++c) {
+    int r0, r1;
+    cta_rows(c, L.G, L.V, L.unit_rows, r0, r1);
+    if (r0 >= e) break;
+    const int s0 = c * L.max_seg * 8, s1 = s0 + L.max_seg * 8;
+    for (int s = s0; s < s1; ++s)
+      if (part_group[s] == k) acc = state_merge(acc, part[(size_t)s * B + b]);
+  }
+  return acc;
+}
+
+// Grouped variant (§4.1, App. E): one block per batch row, one thread per group.
+__global__ void __launch_bounds__(kReduceThreads)
+reduce_groups_kernel(const State* __restrict__ part, const int* __restrict__ part_group, const SlotLayout L,
+                     int B, int n_groups, int32_t* idx_out, float* score_out, float* logZ_out,
+                     fs_summary* groups_out) {
+  __shared__ State red[kReduceThreads];
+  sm100::pdl_wait();
+  const int b = blockIdx.x, tid = threadIdx.x;
+  State acc = state_empty();
+  for (int k = tid; k < n_groups; k += kReduceThreads) {
+    const State g = merge_group(part, part_group, L, B, b, k);
+    if (groups_out) groups_out[(size_t)b * n_groups + k] = to_summary(g);
+    acc = state_merge(acc, g);
   }
   red[tid] = acc;
   __syncthreads();
@@ -68,7 +123,6 @@ reduce_kernel(const State* __restrict__ part, const int* __restrict__ part_group
     if (idx_out) idx_out[b] = f.idx;
     if (score_out) score_out[b] = f.max_score;
     if (logZ_out) logZ_out[b] = f.log_mass;
-    if (n_groups == 1 && groups_out) groups_out[b] = f;
   }
 }
 
@@ -107,25 +161,25 @@ __global__ void gumbel_kernel(const uint32_t* r, float* g, int64_t n) {
     g[i] = gumbel32(r[i]);
 }
 
-cudaError_t launch_reduce(const State* part, const int* part_group, int n_slots, int B, int n_groups,
+cudaError_t launch_reduce(const State* part, const int* part_group, const SlotLayout& lay, int B, int n_groups,
                           int32_t* idx_out, float* score_out, float* logZ_out, fs_summary* groups_out,
                           cudaStream_t stream, bool pdl) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(B);
-  cfg.blockDim = dim3(kReduceThreads);
-  cfg.dynamicSmemBytes = (size_t)n_slots * sizeof(int);
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  if (cfg.dynamicSmemBytes > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)cfg.dynamicSmemBytes);
-    if (e != cudaSuccess) return e;
+  if (n_groups == 1) {
+    cfg.gridDim = dim3((B + 3) / 4);
+    cfg.blockDim = dim3(128);
+    return cudaLaunchKernelEx(&cfg, reduce_rows_kernel, part, part_group, lay.n_slots, B, idx_out, score_out,
+                              logZ_out, groups_out);
   }
-  return cudaLaunchKernelEx(&cfg, reduce_kernel, part, part_group, n_slots, B, n_groups, idx_out, score_out,
+  cfg.gridDim = dim3(B);
+  cfg.blockDim = dim3(kReduceThreads);
+  return cudaLaunchKernelEx(&cfg, reduce_groups_kernel, part, part_group, lay, B, n_groups, idx_out, score_out,
                             logZ_out, groups_out);
 }
 

@@ -44,10 +44,13 @@ struct fs_ctx {
   int stages_override = 0;
   int kbps = 0;                    // 0 = default
   int dbg_no_mma = 0;
+  int dbg_no_epi = 0;
   int l2promo = 3;                 // CUtensorMapL2promotion for W/h maps (3 = 256B)
   int w_policy = 1;                // 1: W loads evict_first, 0: no cache hint
   int epi_sleep = 0;               // ns of backoff in epilogue barrier waits (0 = spin)
   int unit_rows = 0;               // CTA range granularity (0 = default)
+  int pair = -1;                   // CTA-pair kernel: -1 auto (by batch size), 0 off, 1 on
+  int pair_min_bn = 32;            // auto: use the pair kernel from this MMA N upwards (measured)
   // tensor-map cache: encoding costs host microseconds per map; W maps are reused across calls
   struct MapKey { const void* base; int64_t inner, rows; int box, promo; };
   struct MapEnt { MapKey k; CUtensorMap m; };
@@ -183,17 +186,22 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
   const size_t esz = a.dtype == FS_BF16 ? 2 : 4;
   const int unit = ctx->unit_rows > 0 ? ctx->unit_rows : 16;
   const int U = (a.V + unit - 1) / unit;
-  int G = std::min(ctx->max_ctas > 0 ? ctx->max_ctas : ctx->num_sms, U);
+  const int BN_first = fs::tc_block_n(std::min(a.B, 256));
+  const bool pair = tc && (ctx->pair == 1 || (ctx->pair < 0 && BN_first >= ctx->pair_min_bn)) &&
+                    (ctx->max_ctas > 0 ? ctx->max_ctas : ctx->num_sms) >= 2;
+  // persistent grid: #SMs CTAs (or #SMs/2 pairs), never more work units than rows allow
+  const int units = std::min(std::max(1, (ctx->max_ctas > 0 ? ctx->max_ctas : ctx->num_sms) / (pair ? 2 : 1)), U);
+  const int G = units * (pair ? 2 : 1);
   int max_seg = 1, n_slots;
   const CUtensorMap* wmaps = nullptr;
   if (tc) {
-    fs_status st0 = segment_maps(ctx, a.W, a.D, a.V, G, unit, std::min(a.group_size, a.V), &wmaps, &max_seg);
+    fs_status st0 = segment_maps(ctx, a.W, a.D, a.V, units, unit, std::min(a.group_size, a.V), &wmaps, &max_seg);
     if (st0 != FS_OK) return st0;
     n_slots = (a.group_size >= a.V) ? G : G * max_seg * fs::tc_slots_per_segment();
   } else {
     n_slots = (a.V + 127) / 128;
   }
-  const fs::SlotLayout lay{n_slots, tc ? 0 : 1, G, a.V, max_seg, a.group_size, unit};
+  const fs::SlotLayout lay{n_slots, tc ? 0 : 1, G, a.V, max_seg, a.group_size, unit, pair ? 1 : 0};
   const int chunk = 256;
   const int Bc_max = std::min(a.B, chunk);
   const size_t part_bytes = (size_t)n_slots * Bc_max * sizeof(fs::State);
@@ -239,23 +247,30 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
     if (tc) {
       const int BN = fs::tc_block_n(Bc);
       // K slices per TMA stage: as many as keep >= 3 stages in flight (more contiguous bytes per
-      // W row per request -> better DRAM row locality; measured on B200).
+      // W row per request; measured on B200).
       p.dbg_no_mma = ctx->dbg_no_mma;
+      p.dbg_no_epi = ctx->dbg_no_epi;
       p.w_policy = ctx->w_policy;
       p.epi_sleep = ctx->epi_sleep;
+      auto stages_for = [&](int k) { return pair ? fs::tc2_stages(BN, k) : fs::tc_stages(BN, k); };
       p.kbps = ctx->kbps;
       if (p.kbps <= 0) {
         p.kbps = 1;
         for (int k = 4; k >= 2; --k)
-          if (fs::tc_stages(BN, k) >= 3) { p.kbps = k; break; }
+          if (stages_for(k) >= 3) { p.kbps = k; break; }
       }
-      p.stages = ctx->stages_override > 0 ? ctx->stages_override : fs::tc_stages(BN, p.kbps);
+      p.stages = ctx->stages_override > 0 ? ctx->stages_override : stages_for(p.kbps);
       if (p.stages < 2) return fail(FS_ERR_INVALID, "K slices per stage too large for shared memory");
       CUtensorMap hmap;
-      if ((st = make_map(ctx, &hmap, p.h, a.D, Bc, BN)) != FS_OK) return st;
+      if ((st = make_map(ctx, &hmap, p.h, a.D, Bc, pair ? BN / 2 : BN)) != FS_OK) return st;
       p.wmaps = wmaps;
-      e = fs::launch_fused_tc(hmap, p, BN, a.lse, G, stream);
-      if (e != cudaSuccess) return cuda_fail(e, "stage-1 tcgen05 kernel launch");
+      if (pair) {
+        e = fs::launch_fused_tc2(hmap, p, BN, a.lse, G, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "stage-1 tcgen05 pair kernel launch");
+      } else {
+        e = fs::launch_fused_tc(hmap, p, BN, a.lse, G, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "stage-1 tcgen05 kernel launch");
+      }
     } else {
       e = fs::launch_fused_simt(p, a.dtype, a.lse, stream);
       if (e != cudaSuccess) return cuda_fail(e, "stage-1 CUDA-core kernel launch");
@@ -345,9 +360,12 @@ fs_status fs_ctx_set_option(fs_ctx* ctx, const char* name, int64_t value) {
   else if (!strcmp(name, "stages")) ctx->stages_override = (int)value;
   else if (!strcmp(name, "kbps")) ctx->kbps = (int)value;
   else if (!strcmp(name, "dbg_no_mma")) ctx->dbg_no_mma = (int)value;
+  else if (!strcmp(name, "dbg_no_epi")) ctx->dbg_no_epi = (int)value;
   else if (!strcmp(name, "l2promo")) ctx->l2promo = (int)value;
   else if (!strcmp(name, "w_policy")) ctx->w_policy = (int)value;
   else if (!strcmp(name, "epi_sleep")) ctx->epi_sleep = (int)value;
+  else if (!strcmp(name, "pair")) ctx->pair = (int)value;
+  else if (!strcmp(name, "pair_min_bn")) ctx->pair_min_bn = (int)value;
   else if (!strcmp(name, "unit_rows")) {
     if (value != 0 && value != 16 && value != 32 && value != 64 && value != 128)
       return fail(FS_ERR_INVALID, "unit_rows must be 0, 16, 32, 64 or 128");

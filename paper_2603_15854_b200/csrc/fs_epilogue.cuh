@@ -24,6 +24,7 @@ struct EpiArgs {
   int B;                    // valid columns in this launch
   int row_offset;           // global batch index of column 0 (RNG counter)
   uint32_t k0, k1, c2, c3;  // Philox key and counter words 2, 3
+  int dbg_skip;             // debug: drain TMEM without computing (bounds the MMA+TMA-only time)
 };
 
 struct RowArgs {
@@ -124,34 +125,62 @@ __device__ __forceinline__ void rotate_states(State (&st)[8]) {
   st[7] = t;
 }
 
-template <bool LSE, bool XFORM>
+// Release of the accumulator buffer after the tile's last TMEM read: every thread arrives on the
+// local barrier (1-CTA kernel, count 128) or lane 0 of each warp arrives on the pair leader's
+// barrier (CTA-pair kernel, count 8); tempty_cluster != 0 selects the latter.
+__device__ __forceinline__ void release_tmem(uint64_t* tempty, uint32_t tempty_cluster, int lane) {
+  sm100::tc_fence_before();
+  if (tempty_cluster) {
+    __syncwarp();
+    if (lane == 0) sm100::mbar_arrive_cluster(tempty_cluster);
+  } else {
+    sm100::mbar_arrive(tempty);
+  }
+}
+
+// NG groups of 8 columns per iteration (NG = 2 doubles the independent work in flight: 4 Philox
+// chains, 16 Gumbel evaluations, 16 warp reductions -- the epilogue is latency-bound at one warp
+// pair per SM sub-partition).  Columns >= B are computed on padding and never stored.
+template <bool LSE, bool XFORM, int NG>
 __device__ __forceinline__ void epi_tile_tc(uint32_t taddr, const RowArgs& ra, const EpiArgs& ea, State (&st)[8],
-                                            int lane, uint64_t* tempty) {
+                                            int lane, uint64_t* tempty, uint32_t tempty_cluster = 0) {
+  constexpr int NC = 8 * NG;
   const int B = ea.B;
   const int nch = (B + 31) >> 5;
 #pragma unroll 1
   for (int c = 0; c < nch; ++c) {
     State own = st[0];
 #pragma unroll 1
-    for (int g = 0; g < 4; ++g) {
+    for (int g = 0; g < 4; g += NG) {
       const int col0 = c * 32 + g * 8;
       if (col0 >= B) break;
-      uint32_t r[8];
-      sm100::tmem_ld_32x32b_x8(taddr + (uint32_t)col0, r);
-      const uint32_t qd = (uint32_t)(ea.row_offset + col0) >> 2;
-      const U4 p0 = philox4x32_10(ra.v_lo, qd, ea.c2, ea.c3, ea.k0, ea.k1);
-      const U4 p1 = philox4x32_10(ra.v_lo, qd + 1u, ea.c2, ea.c3, ea.k0, ea.k1);
-      const float gm[8] = {gumbel32(p0.x), gumbel32(p0.y), gumbel32(p0.z), gumbel32(p0.w),
-                           gumbel32(p1.x), gumbel32(p1.y), gumbel32(p1.z), gumbel32(p1.w)};
-      sm100::tmem_wait_ld();
-      if (col0 + 8 >= B) {                      // last TMEM read of this tile: free the buffer
-        sm100::tc_fence_before();
-        sm100::mbar_arrive(tempty);
-      }
-      uint32_t key[8];
-      float lt[8];
+      uint32_t r[NC];
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj) {
+      for (int i = 0; i < NG; ++i)
+        sm100::tmem_ld_32x32b_x8(taddr + (uint32_t)(col0 + 8 * i), *reinterpret_cast<uint32_t(*)[8]>(&r[8 * i]));
+      if (ea.dbg_skip) {
+        sm100::tmem_wait_ld();
+        if (col0 + NC >= B) release_tmem(tempty, tempty_cluster, lane);
+        if (r[0] == 0x7FFFFFFFu && r[NC - 1] == 0x7FFFFFFFu) own.key = 1u;   // keep the loads live
+        continue;
+      }
+      // randomness first: independent of the accumulator, overlaps the TMEM load
+      const uint32_t qd = (uint32_t)(ea.row_offset + col0) >> 2;
+      float gm[NC];
+#pragma unroll
+      for (int qq = 0; qq < NC / 4; ++qq) {
+        const U4 p4 = philox4x32_10(ra.v_lo, qd + (uint32_t)qq, ea.c2, ea.c3, ea.k0, ea.k1);
+        gm[4 * qq + 0] = gumbel32(p4.x);
+        gm[4 * qq + 1] = gumbel32(p4.y);
+        gm[4 * qq + 2] = gumbel32(p4.z);
+        gm[4 * qq + 3] = gumbel32(p4.w);
+      }
+      sm100::tmem_wait_ld();
+      if (col0 + NC >= B) release_tmem(tempty, tempty_cluster, lane);   // last TMEM read of the tile
+      uint32_t key[NC];
+      float lt[NC];
+#pragma unroll
+      for (int jj = 0; jj < NC; ++jj) {
         float l = __uint_as_float(r[jj]);
         if (XFORM) {
           l = (l + ra.bias) * ea.invtau[col0 + jj];
@@ -164,27 +193,35 @@ __device__ __forceinline__ void epi_tile_tc(uint32_t taddr, const RowArgs& ra, c
         lt[jj] = l;
         key[jj] = ra.valid ? order_key(l + gm[jj]) : kKeyNone;
       }
-      uint32_t kmax[8], ball[8];
+      uint32_t kmax[NC], ball[NC];
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj) kmax[jj] = __reduce_max_sync(0xFFFFFFFFu, key[jj]);
+      for (int jj = 0; jj < NC; ++jj) kmax[jj] = __reduce_max_sync(0xFFFFFFFFu, key[jj]);
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj) ball[jj] = __ballot_sync(0xFFFFFFFFu, key[jj] == kmax[jj]);
-      float Sw[8];
+      for (int jj = 0; jj < NC; ++jj) ball[jj] = __ballot_sync(0xFFFFFFFFu, key[jj] == kmax[jj]);
+      if (LSE) {
+        float Sw[NC];
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj) {
-        Sw[jj] = 0.0f;
-        if (LSE) {
+        for (int jj = 0; jj < NC; ++jj) {
           const float m = key_ref(kmax[jj]);
           float e = (ra.valid && m != -INFINITY) ? fast_exp2((lt[jj] - m) * kLog2e) : 0.0f;
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xFFFFFFFFu, e, o);
           Sw[jj] = e;
         }
-      }
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj)
-        if (lane == g * 8 + jj)
-          absorb<LSE>(own, kmax[jj], kmax[jj] > kKeyNone ? ra.warp_v0 + (__ffs(ball[jj]) - 1) : -1, Sw[jj]);
+        for (int jj = 0; jj < NC; ++jj)
+          if (lane == g * 8 + jj)
+            absorb<true>(own, kmax[jj], kmax[jj] > kKeyNone ? ra.warp_v0 + (__ffs(ball[jj]) - 1) : -1, Sw[jj]);
+      } else {
+        // branch-free: the owner lane of column jj keeps the larger key (ties keep the earlier id)
+#pragma unroll
+        for (int jj = 0; jj < NC; ++jj) {
+          const int32_t widx = ra.warp_v0 + (__ffs(ball[jj]) - 1);
+          const bool upd = (lane == g * 8 + jj) && (kmax[jj] > own.key);
+          own.key = upd ? kmax[jj] : own.key;
+          own.idx = upd ? widx : own.idx;
+        }
+      }
     }
     st[0] = own;
     if (nch > 1) rotate_states(st);

@@ -177,6 +177,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
     ea.k1 = (uint32_t)(p.seed >> 32);
     ea.c2 = ctr_step_lo(p.step);
     ea.c3 = ctr_step_hi(p.step, 0u);
+    ea.dbg_skip = p.dbg_no_epi;
     State st[8];
 #pragma unroll
     for (int c = 0; c < 8; ++c) st[c] = state_empty();
@@ -199,7 +200,8 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
         ra.warp_v0 = (int32_t)(p.vocab_offset + t0 + 32 * q);
         ra.bias = (XFORM && ra.valid && p.bias) ? p.bias[row] : 0.0f;
         const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(set * BN);
-        epi_tile_tc<LSE, XFORM>(taddr, ra, ea, st, lane, &tempty[set]);
+        if (p.B <= 8) epi_tile_tc<LSE, XFORM, 1>(taddr, ra, ea, st, lane, &tempty[set]);
+        else epi_tile_tc<LSE, XFORM, 2>(taddr, ra, ea, st, lane, &tempty[set]);
       }
       if (gs < p.V) {                           // grouped: one candidate slot per (segment, warp)
         const int slot = (slot0 + seg) * kEpiWarps + e;

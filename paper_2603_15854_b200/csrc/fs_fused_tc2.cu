@@ -1,0 +1,280 @@
+// fs_fused_tc2.cu -- stage 1 of FlashSampling on a CTA PAIR (tcgen05 cta_group::2).
+//
+// Same contract and epilogue as fs_fused_tc.cu, for larger batches.  Two CTAs of a cluster
+// (one TPC) compute an M=256 x N=BN x K=16 MMA per instruction: CTA r holds W rows
+// [t0 + 128 r, t0 + 128 r + 128) of each 256-row tile (the A operand, split by M) and batch rows
+// [r BN/2, (r+1) BN/2) of h (the B operand, split by N); each CTA's TMEM receives its 128 rows
+// x all BN columns.  Per W byte a CTA now moves half as many h bytes through its TMA ring and
+// shared memory as the 1-CTA kernel (at B=256: 1x instead of 2x the W bytes), which is what
+// limits the 1-CTA kernel at B >= 128.
+//
+// Synchronisation (leader = even CTA, issues all MMAs):
+//   full[s]    leader's barrier; both CTAs' 2-SM TMA loads complete_tx on it (peer bit cleared);
+//              the leader's producer arms it with the pair's byte count.
+//   empty[s]   one per CTA, arrived by the leader's multicast tcgen05.commit.
+//   tfull[b]   one per CTA, arrived by the multicast commit after a tile's last MMA.
+//   tempty[b]  leader's barrier, 8 arrivals: lane 0 of the 4 epilogue warps of set b in each CTA.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "fs_epilogue.cuh"
+#include "fs_kernels.h"
+
+namespace fs {
+
+namespace {
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr int kBlockK = 64;
+constexpr int kWBytes = 128 * kBlockK * 2;                  // this CTA's 128 W rows per K slice
+constexpr int kExtraBytes = 64 * 8 + 16 + 256 * 4 + 64;
+
+int tmem_cols_for(int BN) {
+  int c = 32;
+  while (c < 2 * BN) c <<= 1;
+  return c;
+}
+__device__ __forceinline__ int seg_end2(int a, int r1, int gs) { return min(r1, (a / gs + 1) * gs); }
+}  // namespace
+
+template <bool LSE, bool XFORM>
+__global__ void __launch_bounds__(kThreads, 1)
+fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int S = p.stages, BN = p.bn, KBPS = p.kbps;
+  const int h_bytes = (BN / 2) * kBlockK * 2;                 // this CTA's half of h per K slice
+  uint8_t* w_ring = smem;
+  uint8_t* h_ring = smem + (size_t)S * KBPS * kWBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(h_ring + (size_t)S * KBPS * h_bytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* invtau = reinterpret_cast<float*>(tmem_slot + 4);
+
+  const uint32_t rank = sm100::cluster_ctarank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const CUtensorMap* wmaps = p.wmaps + (size_t)pair * p.max_seg;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    sm100::prefetch_tmap(&tmH);
+    for (int s = 0; s < p.max_seg; ++s) sm100::prefetch_tmap(&wmaps[s]);
+    for (int s = 0; s < S; ++s) {
+      sm100::mbar_init(&full[s], 1);
+      sm100::mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&tfull[i], 1);
+      sm100::mbar_init(&tempty[i], 8);
+    }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 1) sm100::tmem_alloc_pair(tmem_slot, (uint32_t)p.tmem_cols);
+  if (XFORM) {
+    for (int b = threadIdx.x; b < 256; b += kThreads) {
+      float it = __int_as_float(0x7FC00000);
+      if (b < p.B) {
+        const float t = p.temperature ? p.temperature[b] : 1.0f;
+        if (t > 0.0f && isfinite(t)) it = 1.0f / t;
+      }
+      invtau[b] = it;
+    }
+  }
+  sm100::tc_fence_before();
+  sm100::cluster_sync();                    // both CTAs' barriers exist before any remote signal
+  sm100::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  sm100::pdl_launch_dependents();
+
+  int r0, r1;
+  cta_rows(pair, npairs, p.V, p.unit_rows, r0, r1);
+  const int num_kb = (p.D + kBlockK - 1) / kBlockK;
+  const int gs = p.group_size;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // -------------------------- TMA producer (both CTAs) ------------------------------
+      const uint64_t pol_w = p.w_policy ? sm100::policy_evict_first() : sm100::policy_evict_normal();
+      const uint64_t pol_h = sm100::policy_evict_last();
+      const uint32_t pair_tx = 2u * (uint32_t)(kWBytes + h_bytes);
+      int stage = 0;
+      uint32_t phase = 0;
+      int seg = 0;
+      for (int a = r0; a < r1; ++seg) {
+        const int b = seg_end2(a, r1, gs);
+        const CUtensorMap* wm = &wmaps[seg];
+        for (int t0 = a; t0 < b; t0 += 256) {
+          for (int kb0 = 0; kb0 < num_kb; kb0 += KBPS) {
+            const int nk = min(KBPS, num_kb - kb0);
+            sm100::mbar_wait(&empty[stage], phase ^ 1);
+            if (rank == 0) sm100::mbar_arrive_expect_tx(&full[stage], pair_tx * nk);
+            for (int j = 0; j < nk; ++j) {
+              const int kb = kb0 + j;
+              sm100::tma_load_2d_pair(w_ring + ((size_t)stage * KBPS + j) * kWBytes, wm, &full[stage], kb * kBlockK,
+                                      t0 - a + 128 * (int)rank, pol_w);
+              sm100::tma_load_2d_pair(h_ring + ((size_t)stage * KBPS + j) * h_bytes, &tmH, &full[stage],
+                                      kb * kBlockK, (int)rank * (BN / 2), pol_h);
+            }
+            if (++stage == S) { stage = 0; phase ^= 1; }
+          }
+        }
+        a = b;
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // -------------------------- MMA issuer (leader only) ------------------------------
+      const uint32_t idesc = sm100::umma_idesc_bf16(256, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int tile_i = 0;
+      for (int a = r0; a < r1;) {
+        const int b = seg_end2(a, r1, gs);
+        for (int t0 = a; t0 < b; t0 += 256, ++tile_i) {
+          const int buf = tile_i & 1;
+          const uint32_t use = (uint32_t)(tile_i >> 1);
+          sm100::mbar_wait(&tempty[buf], (use & 1) ^ 1);
+          sm100::tc_fence_after();
+          const uint32_t d_tmem = tmem_base + (uint32_t)(buf * BN);
+          for (int kb0 = 0; kb0 < num_kb; kb0 += KBPS) {
+            const int nk = p.dbg_no_mma ? 0 : min(KBPS, num_kb - kb0);
+            sm100::mbar_wait(&full[stage], phase);
+            sm100::tc_fence_after();
+            for (int j = 0; j < nk; ++j) {
+              const uint64_t adesc =
+                  sm100::umma_desc_sw128(sm100::smem_u32(w_ring + ((size_t)stage * KBPS + j) * kWBytes));
+              const uint64_t bdesc =
+                  sm100::umma_desc_sw128(sm100::smem_u32(h_ring + ((size_t)stage * KBPS + j) * h_bytes));
+#pragma unroll
+              for (int k = 0; k < kBlockK / 16; ++k)
+                sm100::mma_bf16_ss_pair(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, ((kb0 + j) | k) != 0 ? 1u : 0u);
+            }
+            sm100::mma_commit_pair(&empty[stage], 0x3);
+            if (++stage == S) { stage = 0; phase ^= 1; }
+          }
+          sm100::mma_commit_pair(&tfull[buf], 0x3);
+        }
+        a = b;
+      }
+    }
+  } else {
+    // -------------------------------- epilogue (both CTAs) ------------------------------
+    const int e = warp - 2;
+    const int set = e >> 2;
+    const int q = warp & 3;
+    EpiArgs ea;
+    ea.invtau = invtau;
+    ea.mask = p.mask;
+    ea.mask_words = p.mask_words;
+    ea.B = p.B;
+    ea.row_offset = p.row_offset;
+    ea.k0 = (uint32_t)p.seed;
+    ea.k1 = (uint32_t)(p.seed >> 32);
+    ea.c2 = ctr_step_lo(p.step);
+    ea.c3 = ctr_step_hi(p.step, 0u);
+    ea.dbg_skip = p.dbg_no_epi;
+    const uint32_t tempty_leader = sm100::mapa(sm100::smem_u32(&tempty[set]), 0);
+    State st[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) st[c] = state_empty();
+    const int slot0 = blockIdx.x * p.max_seg;
+    int tile_i = 0, seg = 0;
+    for (int a = r0; a < r1; ++seg) {
+      const int b = seg_end2(a, r1, gs);
+      for (int t0 = a; t0 < b; t0 += 256, ++tile_i) {
+        if ((tile_i & 1) != set) continue;
+        const uint32_t use = (uint32_t)(tile_i >> 1);
+        sm100::mbar_wait(&tfull[set], use & 1);
+        sm100::tc_fence_after();
+        const int base = t0 + 128 * (int)rank;
+        const int row = base + 32 * q + lane;
+        RowArgs ra;
+        ra.valid = row < b;
+        ra.v_global = (int32_t)(p.vocab_offset + row);
+        ra.v_lo = (uint32_t)ra.v_global;
+        ra.warp_v0 = (int32_t)(p.vocab_offset + base + 32 * q);
+        ra.bias = (XFORM && ra.valid && p.bias) ? p.bias[row] : 0.0f;
+        const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(set * BN);
+        if (p.B <= 8) epi_tile_tc<LSE, XFORM, 1>(taddr, ra, ea, st, lane, &tempty[set], tempty_leader);
+        else epi_tile_tc<LSE, XFORM, 2>(taddr, ra, ea, st, lane, &tempty[set], tempty_leader);
+      }
+      if (gs < p.V) {
+        const int slot = (slot0 + seg) * kEpiWarps + e;
+        flush_warp(st, lane, p.B, p.part + (size_t)slot * p.B);
+        if (lane == 0) p.part_group[slot] = a / gs;
+      }
+      a = b;
+    }
+    if (gs < p.V) {
+      if (lane == 0)
+        for (int s = seg; s < p.max_seg; ++s) p.part_group[(slot0 + s) * kEpiWarps + e] = -1;
+    } else {
+      // all tiles drained -> this CTA's ring is free (the leader's MMAs no longer read it)
+      sm100::named_bar_sync(1, 32 * kEpiWarps);
+      State* scratch = reinterpret_cast<State*>(w_ring);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int bb = c * 32 + lane;
+        if (bb < BN) scratch[e * BN + bb] = st[c];
+      }
+      sm100::named_bar_sync(1, 32 * kEpiWarps);
+      const int et = threadIdx.x - 64;
+      for (int bb = et; bb < p.B; bb += 32 * kEpiWarps) {
+        State m = scratch[bb];
+#pragma unroll
+        for (int w = 1; w < kEpiWarps; ++w) m = state_merge(m, scratch[w * BN + bb]);
+        p.part[(size_t)blockIdx.x * p.B + bb] = m;
+      }
+      if (et == 0) p.part_group[blockIdx.x] = (r0 < r1) ? 0 : -1;
+    }
+  }
+
+  sm100::tc_fence_before();
+  sm100::cluster_sync();                    // no remote arrivals / MMAs into our TMEM after this
+  if (warp == 1) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc_pair(tmem_base, (uint32_t)p.tmem_cols);
+  }
+}
+
+int tc2_stages(int BN, int kbps) {
+  const int budget = 227 * 1024 - 1024;
+  const int stage = (kWBytes + (BN / 2) * kBlockK * 2) * kbps;
+  int S = 16;
+  while (S > 0 && S * stage + kExtraBytes > budget) --S;
+  return S;
+}
+
+cudaError_t launch_fused_tc2(const CUtensorMap& hmap, const StageOneParams& p_in, int BN, bool lse, int grid,
+                             cudaStream_t stream) {
+  StageOneParams p = p_in;
+  p.bn = BN;
+  p.tmem_cols = tmem_cols_for(BN);
+  const size_t smem = 1024 + (size_t)p.stages * p.kbps * (kWBytes + (BN / 2) * kBlockK * 2) + kExtraBytes;
+  const bool xform = p.bias || p.temperature || p.mask;
+  auto kern = lse ? (xform ? fused_tc2_kernel<true, true> : fused_tc2_kernel<true, false>)
+                  : (xform ? fused_tc2_kernel<false, true> : fused_tc2_kernel<false, false>);
+  static bool attr_set[4] = {false, false, false, false};
+  const int variant = (lse ? 2 : 0) + (xform ? 1 : 0);
+  if (!attr_set[variant]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_set[variant] = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, hmap, p);
+}
+
+}  // namespace fs

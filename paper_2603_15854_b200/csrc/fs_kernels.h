@@ -28,6 +28,7 @@ struct StageOneParams {
   int unit_rows;              // CTA range granularity in rows (TC kernel): 16, 32, 64 or 128
   int kbps;                   // 64-wide K slices per ring stage (TC kernel)
   int dbg_no_mma;             // debug: stream operands through the ring without issuing MMAs
+  int dbg_no_epi;             // debug: epilogue drains TMEM without computing
   int w_policy;               // 1: W TMA loads carry an L2 evict_first hint
   int epi_sleep;              // ns backoff while epilogue warps wait for an accumulator
   int bn;                     // MMA N (batch columns, padded) (TC kernel; set by launch_fused_tc)
@@ -41,6 +42,10 @@ struct StageOneParams {
 int tc_block_n(int B);
 int tc_stages(int BN, int kbps);
 int tc_slots_per_segment();   // candidate slots one CTA writes per group segment
+int tc2_stages(int BN, int kbps);
+// CTA-pair (cta_group::2) stage 1: grid = 2 x pairs, cluster (2,1,1); h map box = BN/2 rows.
+cudaError_t launch_fused_tc2(const CUtensorMap& hmap, const StageOneParams& p, int BN, bool lse, int grid,
+                             cudaStream_t stream);
 cudaError_t launch_fused_tc(const CUtensorMap& hmap, const StageOneParams& p, int BN, bool lse, int grid,
                             cudaStream_t stream);
 // CUDA-core stage 1: grid = ceil(V/128) aligned tiles, one slot per tile.
@@ -55,6 +60,7 @@ struct SlotLayout {
   int max_seg;       // tcgen05 grouped: segments per CTA (slot = (cta*max_seg + seg)*8 + warp)
   int group_size;
   int unit_rows;     // tcgen05: CTA range granularity
+  int pair;          // tcgen05: 1 if the partition is over CTA pairs (cta_group::2 kernel)
 };
 
 // Stage 2: reduce the candidate slots of every row into groups and the final sample.

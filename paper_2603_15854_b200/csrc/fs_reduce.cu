@@ -79,21 +79,26 @@ __device__ __forceinline__ State merge_group(const State* __restrict__ part, con
     for (int t = a / 128; t < (e + 127) / 128; ++t) acc = state_merge(acc, part[(size_t)t * B + b]);
     return acc;
   }
-  // first CTA with r1 > a, last CTA with r0 < e
-  int lo = 0, hi = L.G - 1;
+  // partition units are CTAs, or CTA pairs for the cta_group::2 kernel
+  const int units = L.pair ? L.G / 2 : L.G;
+  const int per = L.pair ? 2 : 1;
+  // first unit with r1 > a, then every unit with r0 < e
+  int lo = 0, hi = units - 1;
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
     int r0, r1;
-    cta_rows(mid, L.G, L.V, L.unit_rows, r0, r1);
+    cta_rows(mid, units, L.V, L.unit_rows, r0, r1);
     if (r1 > a) hi = mid; else lo = mid + 1;
   }
-  for (int c = lo; c < L.G; ++c) {
+  for (int u = lo; u < units; ++u) {
     int r0, r1;
-    cta_rows(c, L.G, L.V, L.unit_rows, r0, r1);
+    cta_rows(u, units, L.V, L.unit_rows, r0, r1);
     if (r0 >= e) break;
-    const int s0 = c * L.max_seg * 8, s1 = s0 + L.max_seg * 8;
-    for (int s = s0; s < s1; ++s)
-      if (part_group[s] == k) acc = state_merge(acc, part[(size_t)s * B + b]);
+    for (int c = u * per; c < (u + 1) * per; ++c) {
+      const int s0 = c * L.max_seg * 8, s1 = s0 + L.max_seg * 8;
+      for (int s = s0; s < s1; ++s)
+        if (part_group[s] == k) acc = state_merge(acc, part[(size_t)s * B + b]);
+    }
   }
   return acc;
 }

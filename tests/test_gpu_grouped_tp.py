@@ -116,3 +116,26 @@ def test_merge_summaries_online():
     torch.cuda.synchronize()
     assert torch.equal(run.idx, idx)
     assert torch.allclose(run.log_mass, logZ, atol=1e-4)
+
+
+@pytest.fixture
+def pair_on():
+    fs.set_option("pair", 1)
+    yield
+    fs.set_option("pair", -1)
+
+
+def test_grouped_and_tp_on_cta_pairs(pair_on):
+    wl = synth.make_workload("gemma3_27b", 40, V=9000, D=128, with_transforms=True)
+    h, W, bias, tau, mask = (x.cuda() for x in (wl.h, wl.W, wl.bias, wl.temperature, wl.mask))
+    idx, score, logZ, groups = fs.sample_grouped(h, W, group_size=1024, bias=bias, temperature=tau, mask=mask,
+                                                 seed=wl.seed, step=2)
+    fidx, fscore = fs.sample(h, W, bias=bias, temperature=tau, mask=mask, seed=wl.seed, step=2, return_score=True)
+    assert torch.equal(idx, fidx) and torch.equal(score, fscore)
+    sc, flat = oracle_flat(wl, 2)
+    check_flat(idx.cpu().numpy(), score.cpu().numpy(), flat)
+    _groups_vs_oracle(groups, sc, 1024)
+    parts = [fs.sample_shard(h, W[a:b].contiguous(), a, wl.V, bias_shard=bias[a:b].contiguous(), temperature=tau,
+                             mask=mask, seed=wl.seed, step=2).raw for a, b in sampler.shard_bounds(wl.V, 4)]
+    tidx, tscore, _ = fs.combine_summaries(torch.stack(parts), return_all=True)
+    assert torch.equal(tidx, fidx) and torch.equal(tscore, fscore)

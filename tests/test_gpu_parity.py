@@ -33,7 +33,7 @@ def _run(wl, step, **kw):
 def _reset_options():
     yield
     if torch.cuda.is_available():
-        for k, v in (("force_simt", 0), ("max_ctas", 0), ("pdl", 1), ("stages", 0)):
+        for k, v in (("force_simt", 0), ("max_ctas", 0), ("pdl", 1), ("stages", 0), ("pair", -1), ("kbps", 0)):
             fs.set_option(k, v)
 
 
@@ -160,3 +160,27 @@ def test_cuda_graph_capture_replay():
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(idx, ref)
+
+
+@pytest.mark.parametrize("B", [1, 16, 40, 100, 128, 200, 256])
+def test_cta_pair_kernel_matches_oracle_and_single_cta(B):
+    # cta_group::2 (M=256) kernel vs oracle, and bit-identical to the 1-CTA kernel
+    wl = synth.make_workload("llama3_8b", B, V=5000 + B, D=320, seed_offset=1000 + B)
+    fs.set_option("pair", 0)
+    ref = _run(wl, 6)
+    fs.set_option("pair", 1)
+    got = _run(wl, 6)
+    assert np.array_equal(got[0], ref[0])
+    assert np.array_equal(got[1].view(np.uint32), ref[1].view(np.uint32))
+    _, flat = oracle_flat(wl, 6)
+    check_flat(*got, flat)
+
+
+@pytest.mark.parametrize("max_ctas", [2, 6, 38, 0])
+def test_cta_pair_grid_invariance(max_ctas):
+    wl = synth.make_workload("qwen25_7b", 64, V=9000, D=192)
+    ref = _run(wl, 2)
+    fs.set_option("pair", 1)
+    fs.set_option("max_ctas", max_ctas)
+    got = _run(wl, 2)
+    assert np.array_equal(got[0], ref[0]) and np.array_equal(got[1], ref[1])

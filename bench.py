@@ -186,9 +186,12 @@ def fused_step_fn(fs, wl, step_ctr, out):
 
 def baselines(wl, iters, warmup):
     """Unfused paths on the same inputs: cuBLAS GEMM alone; GEMM + softmax +
-    torch.multinomial (eager); FlashInfer FI2 (Gumbel-max on logits) and FI1 (top-k/top-p)."""
+    torch.multinomial (eager); FlashInfer FI2 (Gumbel-max on logits) and FI1 (top-k/top-p).
+    For the grouped workload the unfused path must also produce the log-normalizer and the
+    per-group log-masses (torch.logsumexp over the materialised logits)."""
     h, W, bias, tau, mask = wl["h"], wl["W"], wl["bias"], wl["temperature"], wl["mask"]
     V = W.shape[0]
+    g = wl["group_size"]
     res = {}
 
     def transformed():
@@ -202,15 +205,27 @@ def baselines(wl, iters, warmup):
             lg = lg.masked_fill(~allowed, float("-inf"))
         return lg
 
+    def with_groups(sampler_fn):
+        def fn():
+            lg = transformed()
+            out = sampler_fn(lg)
+            if g:
+                pad = (-V) % g
+                lgp = torch.nn.functional.pad(lg, (0, pad), value=float("-inf"))
+                torch.logsumexp(lgp.view(lg.shape[0], -1, g), dim=-1)
+                torch.logsumexp(lg, dim=-1)
+            return out
+        return fn
+
     res["cublas_gemm_only_us"] = 1e3 * time_median(lambda: torch.matmul(h, W.t()), iters, warmup)
     res["gemm_softmax_multinomial_eager_us"] = 1e3 * time_median(
-        lambda: torch.multinomial(torch.softmax(transformed(), -1), 1), iters, warmup)
+        with_groups(lambda lg: torch.multinomial(torch.softmax(lg, -1), 1)), iters, warmup)
     try:
         import flashinfer.sampling as fis
         res["fi2_gemm_sampling_from_logits_us"] = 1e3 * time_median(
-            lambda: fis.sampling_from_logits(transformed()), iters, warmup)
+            with_groups(lambda lg: fis.sampling_from_logits(lg)), iters, warmup)
         res["fi1_gemm_top_k_top_p_us"] = 1e3 * time_median(
-            lambda: fis.top_k_top_p_sampling_from_logits(transformed(), 50, 0.95), iters, warmup)
+            with_groups(lambda lg: fis.top_k_top_p_sampling_from_logits(lg, 50, 0.95)), iters, warmup)
     except Exception as e:  # pragma: no cover - FlashInfer missing or failing on this box
         res["flashinfer_error"] = repr(e)[:200]
     return res
@@ -360,6 +375,10 @@ def run_single(args):
                     "d2h_bytes_per_step": B * 4}}
     if not args.no_sweep:
         line["sweep"] = sweep(fs, name, pk, args)
+        # the other BASELINE.json configs (same protocol): transforms, grouped, 70B LM head
+        if name == "llama3_8b" and not args.no_configs:
+            line["configs"] = {c: sweep(fs, c, pk, args, Bs=(1, 32, 256))
+                               for c in ("qwen25_7b", "gemma3_27b", "llama3_70b")}
     if not args.no_cpu:
         cus, cores, sample = cpu_oracle_step_us(name, B, args.cpu_seconds)
         line["cpu_baseline"] = {"value": round(cus, 1), "unit": UNIT, "cores": cores, "kind": "oracle",
@@ -367,10 +386,10 @@ def run_single(args):
     print(json.dumps(line), flush=True)
 
 
-def sweep(fs, name, pk, args):
+def sweep(fs, name, pk, args, Bs=(1, 8, 32, 128, 256)):
     res = {}
     dev = torch.device("cuda", 0)
-    for B in (1, 8, 32, 128, 256):
+    for B in Bs:
         wl = make_device_workload(name, B, dev, seed=99 + B)
         D, V = wl["D"], wl["V"]
         transforms = wl["bias"] is not None
@@ -385,7 +404,7 @@ def sweep(fs, name, pk, args):
         fs.set_option("time_stage1", 0)
         r = {"fused_us": round(us, 2), "stage1_us": round(t1 * 1e3, 2)}
         r["roofline"] = roofline(name, B, D, V, t1, pk, transforms)
-        if not args.no_baselines and not wl["group_size"]:
+        if not args.no_baselines:
             bl = baselines(wl, 100, 25)
             r["baselines"] = {k: (round(v, 2) if isinstance(v, float) else v) for k, v in bl.items()}
             unfused = [v for k, v in bl.items() if k.endswith("_us") and k != "cublas_gemm_only_us"]
@@ -494,6 +513,7 @@ def main():
     ap.add_argument("--B", type=int, default=32)
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-baselines", action="store_true")
+    ap.add_argument("--no-configs", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     args = ap.parse_args()

@@ -164,7 +164,17 @@ __device__ __forceinline__ void epi_tile_tc(uint32_t taddr, const RowArgs& ra, c
         if (r[0] == 0x7FFFFFFFu && r[NC - 1] == 0x7FFFFFFFu) own.key = 1u;   // keep the loads live
         continue;
       }
-      // randomness first: independent of the accumulator, overlaps the TMEM load
+      // mask words for these columns: lane j < 16 holds word (col0+j, w0), lane 16+j word
+      // (col0+j, w0+1), w0 = first word of the warp's 32 rows (rows may straddle two words)
+      uint32_t mw = 0xFFFFFFFFu;
+      const int wshift = ra.warp_v0 & 31;
+      if (XFORM && ea.mask != nullptr) {
+        const int jb = col0 + (lane & 15);
+        const int64_t w = (int64_t)(ra.warp_v0 >> 5) + (lane >> 4);
+        mw = 0u;
+        if ((lane & 15) < NC && jb < B && w < ea.mask_words) mw = __ldg(ea.mask + (int64_t)jb * ea.mask_words + w);
+      }
+      // randomness: independent of the accumulator, overlaps the TMEM load
       const uint32_t qd = (uint32_t)(ea.row_offset + col0) >> 2;
       float gm[NC];
 #pragma unroll
@@ -184,9 +194,10 @@ __device__ __forceinline__ void epi_tile_tc(uint32_t taddr, const RowArgs& ra, c
         float l = __uint_as_float(r[jj]);
         if (XFORM) {
           l = (l + ra.bias) * ea.invtau[col0 + jj];
-          if (ea.mask != nullptr && col0 + jj < B) {
-            const uint32_t w = __ldg(ea.mask + (int64_t)(col0 + jj) * ea.mask_words + (ra.v_global >> 5));
-            if (!((w >> (ra.v_global & 31)) & 1u)) l = -INFINITY;
+          if (ea.mask != nullptr) {
+            const uint32_t lo = __shfl_sync(0xFFFFFFFFu, mw, jj), hi = __shfl_sync(0xFFFFFFFFu, mw, 16 + jj);
+            const uint32_t bits = wshift ? __funnelshift_r(lo, hi, wshift) : lo;
+            if (!((bits >> lane) & 1u)) l = -INFINITY;
           }
         }
         if (isnan(l)) l = -INFINITY;
@@ -198,29 +209,55 @@ __device__ __forceinline__ void epi_tile_tc(uint32_t taddr, const RowArgs& ra, c
       for (int jj = 0; jj < NC; ++jj) kmax[jj] = __reduce_max_sync(0xFFFFFFFFu, key[jj]);
 #pragma unroll
       for (int jj = 0; jj < NC; ++jj) ball[jj] = __ballot_sync(0xFFFFFFFFu, key[jj] == kmax[jj]);
+      // the owner lane of column col0+jj is g*8+jj: select its column's result (no branches)
+      const int jo = lane - g * 8;
+      uint32_t km = 0u, bl = 0u;
+#pragma unroll
+      for (int jj = 0; jj < NC; ++jj) {
+        km = (jo == jj) ? kmax[jj] : km;
+        bl = (jo == jj) ? ball[jj] : bl;
+      }
+      const int32_t wi = km > kKeyNone ? ra.warp_v0 + (__ffs(bl) - 1) : -1;
+      const bool mine = (unsigned)jo < (unsigned)NC;
       if (LSE) {
-        float Sw[NC];
+        // e = exp(l~ - M_col) per element; warp sums by a reduce-scatter butterfly: after log2(NC)
+        // halving steps lane L holds column L >> (5 - log2 NC), the remaining xor steps finish
+        // the 32-lane sum (2 shuffles per column instead of 5).
+        float ev[NC];
 #pragma unroll
         for (int jj = 0; jj < NC; ++jj) {
           const float m = key_ref(kmax[jj]);
-          float e = (ra.valid && m != -INFINITY) ? fast_exp2((lt[jj] - m) * kLog2e) : 0.0f;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xFFFFFFFFu, e, o);
-          Sw[jj] = e;
+          ev[jj] = (ra.valid && m != -INFINITY) ? fast_exp2((lt[jj] - m) * kLog2e) : 0.0f;
         }
+        int n = NC, bit = 16;
 #pragma unroll
-        for (int jj = 0; jj < NC; ++jj)
-          if (lane == g * 8 + jj)
-            absorb<true>(own, kmax[jj], kmax[jj] > kKeyNone ? ra.warp_v0 + (__ffs(ball[jj]) - 1) : -1, Sw[jj]);
+        for (int st2 = 0; st2 < 4; ++st2) {
+          if (n > 1) {
+            const bool upper = (lane & bit) != 0;
+            const int h2 = n >> 1;
+#pragma unroll
+            for (int i2 = 0; i2 < 8; ++i2) {
+              if (i2 < h2) {
+                const float keep = upper ? ev[h2 + i2] : ev[i2];
+                const float send = upper ? ev[i2] : ev[h2 + i2];
+                ev[i2] = keep + __shfl_xor_sync(0xFFFFFFFFu, send, bit);
+              }
+            }
+            n = h2;
+            bit >>= 1;
+          }
+        }
+        float v = ev[0];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+          if (o <= bit) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+        constexpr int kShift = (NC == 16) ? 1 : 2;          // column of lane L = L >> kShift
+        const float Sw = __shfl_sync(0xFFFFFFFFu, v, (jo & (NC - 1)) << kShift);
+        if (mine) absorb<true>(own, km, wi, Sw);
       } else {
-        // branch-free: the owner lane of column jj keeps the larger key (ties keep the earlier id)
-#pragma unroll
-        for (int jj = 0; jj < NC; ++jj) {
-          const int32_t widx = ra.warp_v0 + (__ffs(ball[jj]) - 1);
-          const bool upd = (lane == g * 8 + jj) && (kmax[jj] > own.key);
-          own.key = upd ? kmax[jj] : own.key;
-          own.idx = upd ? widx : own.idx;
-        }
+        const bool upd = mine && (km > own.key);       // ties keep the earlier (smaller) id
+        own.key = upd ? km : own.key;
+        own.idx = upd ? wi : own.idx;
       }
     }
     st[0] = own;

@@ -211,8 +211,14 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
       a = b;
     }
     if (gs < p.V) {
-      if (lane == 0)
-        for (int s = seg; s < p.max_seg; ++s) p.part_group[(slot0 + s) * kEpiWarps + e] = -1;
+      // unused segment slots: empty candidates tagged with the last group, so that group ids are
+      // non-decreasing over ALL slots (stage 2 finds a group's slots by binary search)
+      const int last_group = (r1 > r0 ? r1 - 1 : r0) / gs;
+      for (int s = seg; s < p.max_seg; ++s) {
+        const int slot = (slot0 + s) * kEpiWarps + e;
+        flush_warp(st, lane, p.B, p.part + (size_t)slot * p.B);
+        if (lane == 0) p.part_group[slot] = last_group;
+      }
     } else {
       // Single group: all tiles are drained, so every MMA has consumed its stage and the TMA
       // ring is free; use it as scratch to merge the 8 warps' candidates into ONE slot per CTA

@@ -178,7 +178,7 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
     State st[8];
 #pragma unroll
     for (int c = 0; c < 8; ++c) st[c] = state_empty();
-    const int slot0 = blockIdx.x * p.max_seg;
+    const int slot0 = pair * p.max_seg;   // slot = ((pair*max_seg + seg)*2 + rank)*8 + warp
     int tile_i = 0, seg = 0;
     for (int a = r0; a < r1; ++seg) {
       const int b = seg_end2(a, r1, gs);
@@ -200,15 +200,21 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
         else epi_tile_tc<LSE, XFORM, 2>(taddr, ra, ea, st, lane, &tempty[set], tempty_leader);
       }
       if (gs < p.V) {
-        const int slot = (slot0 + seg) * kEpiWarps + e;
+        const int slot = ((slot0 + seg) * 2 + (int)rank) * kEpiWarps + e;
         flush_warp(st, lane, p.B, p.part + (size_t)slot * p.B);
         if (lane == 0) p.part_group[slot] = a / gs;
       }
       a = b;
     }
     if (gs < p.V) {
-      if (lane == 0)
-        for (int s = seg; s < p.max_seg; ++s) p.part_group[(slot0 + s) * kEpiWarps + e] = -1;
+      // unused segment slots: empty candidates tagged with the last group, so that group ids are
+      // non-decreasing over ALL slots (stage 2 finds a group's slots by binary search)
+      const int last_group = (r1 > r0 ? r1 - 1 : r0) / gs;
+      for (int s = seg; s < p.max_seg; ++s) {
+        const int slot = ((slot0 + s) * 2 + (int)rank) * kEpiWarps + e;
+        flush_warp(st, lane, p.B, p.part + (size_t)slot * p.B);
+        if (lane == 0) p.part_group[slot] = last_group;
+      }
     } else {
       // all tiles drained -> this CTA's ring is free (the leader's MMAs no longer read it)
       sm100::named_bar_sync(1, 32 * kEpiWarps);

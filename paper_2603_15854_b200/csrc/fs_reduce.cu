@@ -68,54 +68,65 @@ reduce_rows_kernel(const State* __restrict__ part, const int* __restrict__ part_
   }
 }
 
-// Candidate slots of group k: the CTAs whose rows intersect [k g, (k+1) g) (binary search on
-// the persistent partition), each with max_seg x 8 slots tagged by group id.
-__device__ __forceinline__ State merge_group(const State* __restrict__ part, const int* __restrict__ part_group,
-                                             const SlotLayout& L, int B, int b, int k) {
-  State acc = state_empty();
-  const int a = k * L.group_size;
-  const int e = min(L.V, a + L.group_size);
-  if (L.simt) {
-    for (int t = a / 128; t < (e + 127) / 128; ++t) acc = state_merge(acc, part[(size_t)t * B + b]);
-    return acc;
-  }
-  // partition units are CTAs, or CTA pairs for the cta_group::2 kernel
-  const int units = L.pair ? L.G / 2 : L.G;
-  const int per = L.pair ? 2 : 1;
-  // first unit with r1 > a, then every unit with r0 < e
-  int lo = 0, hi = units - 1;
+// Grouped variant (§4.1, App. E): one block per batch row, one thread per group.  Slots are
+// ordered by (unit, segment, warp), so their group ids are non-decreasing: group k's candidates are
+// the contiguous slot range [lower_bound(k), upper_bound(k)), found by binary search over the
+// group ids staged in shared memory; its loads are issued in batches of 8 independent loads.
+__device__ __forceinline__ int lower_bound_smem(const int* a, int n, int key) {
+  int lo = 0, hi = n;
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
-    int r0, r1;
-    cta_rows(mid, units, L.V, L.unit_rows, r0, r1);
-    if (r1 > a) hi = mid; else lo = mid + 1;
+    if (a[mid] < key) lo = mid + 1; else hi = mid;
   }
-  for (int u = lo; u < units; ++u) {
-    int r0, r1;
-    cta_rows(u, units, L.V, L.unit_rows, r0, r1);
-    if (r0 >= e) break;
-    for (int c = u * per; c < (u + 1) * per; ++c) {
-      const int s0 = c * L.max_seg * 8, s1 = s0 + L.max_seg * 8;
-      for (int s = s0; s < s1; ++s)
-        if (part_group[s] == k) acc = state_merge(acc, part[(size_t)s * B + b]);
-    }
-  }
-  return acc;
+  return lo;
 }
 
-// Grouped variant (§4.1, App. E): one block per batch row, one thread per group.
+__device__ __forceinline__ State shfl_xor_state(const State& a, int o) {
+  State r;
+  r.key = __shfl_xor_sync(0xFFFFFFFFu, a.key, o);
+  r.idx = __shfl_xor_sync(0xFFFFFFFFu, a.idx, o);
+  r.S = __shfl_xor_sync(0xFFFFFFFFu, a.S, o);
+  r.pad = 0u;
+  return r;
+}
+
 __global__ void __launch_bounds__(kReduceThreads)
-reduce_groups_kernel(const State* __restrict__ part, const int* __restrict__ part_group, const SlotLayout L,
-                     int B, int n_groups, int32_t* idx_out, float* score_out, float* logZ_out,
-                     fs_summary* groups_out) {
+reduce_groups_kernel(const State* __restrict__ part, const int* __restrict__ part_group, int n_slots, int B,
+                     int n_groups, int32_t* idx_out, float* score_out, float* logZ_out, fs_summary* groups_out) {
+  extern __shared__ int sg[];
   __shared__ State red[kReduceThreads];
   sm100::pdl_wait();
   const int b = blockIdx.x, tid = threadIdx.x;
+  for (int s = tid; s < n_slots; s += kReduceThreads) sg[s] = part_group[s];
+  __syncthreads();
+  // 8 threads per group: thread `sub` merges slots lo+sub, lo+sub+8, ... (one batch of
+  // independent loads), then a fixed xor-shuffle tree combines the 8 partial states.
+  const int sub = tid & 7;
   State acc = state_empty();
-  for (int k = tid; k < n_groups; k += kReduceThreads) {
-    const State g = merge_group(part, part_group, L, B, b, k);
-    if (groups_out) groups_out[(size_t)b * n_groups + k] = to_summary(g);
-    acc = state_merge(acc, g);
+  for (int k0 = 0; k0 < n_groups; k0 += kReduceThreads / 8) {
+    const int k = k0 + (tid >> 3);
+    State g = state_empty();
+    if (k < n_groups) {
+      const int lo = lower_bound_smem(sg, n_slots, k), hi = lower_bound_smem(sg, n_slots, k + 1);
+      for (int s0 = lo + sub; s0 < hi; s0 += 64) {
+        State v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (s0 + 8 * i < hi) v[i] = part[(size_t)(s0 + 8 * i) * B + b];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (s0 + 8 * i < hi) g = state_merge(g, v[i]);
+      }
+    }
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      const State other = shfl_xor_state(g, o);
+      g = (sub & o) ? state_merge(other, g) : state_merge(g, other);
+    }
+    if (sub == 0 && k < n_groups) {
+      if (groups_out) groups_out[(size_t)b * n_groups + k] = to_summary(g);
+      acc = state_merge(acc, g);
+    }
   }
   red[tid] = acc;
   __syncthreads();
@@ -184,8 +195,14 @@ cudaError_t launch_reduce(const State* part, const int* part_group, const SlotLa
   }
   cfg.gridDim = dim3(B);
   cfg.blockDim = dim3(kReduceThreads);
-  return cudaLaunchKernelEx(&cfg, reduce_groups_kernel, part, part_group, lay, B, n_groups, idx_out, score_out,
-                            logZ_out, groups_out);
+  cfg.dynamicSmemBytes = (size_t)lay.n_slots * sizeof(int);
+  if (cfg.dynamicSmemBytes > 40 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(reduce_groups_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)cfg.dynamicSmemBytes);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaLaunchKernelEx(&cfg, reduce_groups_kernel, part, part_group, lay.n_slots, B, n_groups, idx_out,
+                            score_out, logZ_out, groups_out);
 }
 
 cudaError_t launch_combine(const fs_summary* gathered, int n, int B, int32_t* idx_out, float* score_out,

@@ -404,6 +404,28 @@ def sweep(fs, name, pk, args, Bs=(1, 8, 32, 128, 256)):
         fs.set_option("time_stage1", 0)
         r = {"fused_us": round(us, 2), "stage1_us": round(t1 * 1e3, 2)}
         r["roofline"] = roofline(name, B, D, V, t1, pk, transforms)
+        if not args.no_baselines and not wl["group_size"]:
+            # standalone sampling over the same materialised fp32 logits (§5.2):
+            # fs_sample_logits vs FlashInfer's Gumbel-max sampling_from_logits (FI2's sampler)
+            lg = torch.matmul(wl["h"], wl["W"].t()).float()
+            sctr = [0]
+
+            def ours_sl():
+                sctr[0] += 1
+                fs.sample_logits(lg, bias=wl["bias"], temperature=wl["temperature"], mask=wl["mask"],
+                                 seed=synth.SAMPLING_SEED, step=sctr[0])
+            st = {"fs_sample_logits_us": round(1e3 * time_median(ours_sl, 100, 25), 2),
+                  "logits_bytes": lg.numel() * 4}
+            st["fs_sample_logits_gbs"] = round(st["logits_bytes"] / (st["fs_sample_logits_us"] * 1e-6) / 1e9, 1)
+            try:
+                import flashinfer.sampling as fis
+                if wl["bias"] is None:
+                    st["flashinfer_sampling_from_logits_us"] = round(
+                        1e3 * time_median(lambda: fis.sampling_from_logits(lg), 100, 25), 2)
+            except Exception as e:  # pragma: no cover
+                st["flashinfer_error"] = repr(e)[:200]
+            r["standalone_logits"] = st
+            del lg
         if not args.no_baselines:
             bl = baselines(wl, 100, 25)
             r["baselines"] = {k: (round(v, 2) if isinstance(v, float) else v) for k, v in bl.items()}

@@ -111,13 +111,29 @@ fs_status fs_sample(fs_ctx* ctx, fs_dtype dtype,
  * g = group_size, a multiple of 128 (last group ragged).  The outer selection reuses the
  * group maxima (reading R8), so idx_out equals fs_sample's idx_out exactly.
  *   logZ_out   [B] fp32 or NULL: log sum_v exp(l~_v) = logsumexp_k L_k.
- *   groups_out [B][ceil(V/g)] fs_summary or NULL. */
+ *   logprob_out [B] fp32 or NULL: log p(idx) = l~_idx - logZ.
+ *   groups_out [B][ceil(V/g)] fs_summary or NULL.  group_size >= V gives one group (plain
+ *   sampling with logZ / log-probabilities). */
 fs_status fs_sample_grouped(fs_ctx* ctx, fs_dtype dtype,
                             const void* h, const void* W,
                             const float* bias, const float* temperature, const uint32_t* mask,
                             uint64_t seed, uint64_t step, int B, int D, int V, int group_size,
-                            int32_t* idx_out, float* score_out, float* logZ_out,
+                            int32_t* idx_out, float* score_out, float* logZ_out, float* logprob_out,
                             fs_summary* groups_out, void* stream);
+
+/* fs_sample_logits -- standalone FlashSampling over MATERIALISED logits (§5.2; Alg. A.1
+ * P:747-763 parallelised as in Alg. 2): same transform, RNG layout, tie rule and outputs as
+ * fs_sample, for callers that already hold logits (the rival of FlashInfer's
+ * sampling_from_logits).  fs_sample_logits(h W^T) equals fs_sample(h, W) up to the rounding of
+ * the logits themselves.
+ *   logits [B][ld] (dtype bf16 or fp32, row stride ld >= V elements), bias/temperature/mask as above.
+ *   idx_out [B] required; score_out, logZ_out, logprob_out [B] fp32 or NULL, where
+ *   logprob = l~_idx - logZ = log p(idx) (App. E). */
+fs_status fs_sample_logits(fs_ctx* ctx, fs_dtype dtype, const void* logits, int64_t ld,
+                           const float* bias, const float* temperature, const uint32_t* mask,
+                           uint64_t seed, uint64_t step, int B, int V,
+                           int32_t* idx_out, float* score_out, float* logZ_out, float* logprob_out,
+                           void* stream);
 
 /* fs_sample_shard -- the rank-local half of distributed FlashSampling for a vocabulary-
  * sharded (tensor-parallel) LM head (§4.2, Alg. A.4).

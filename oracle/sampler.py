@@ -99,6 +99,30 @@ def scores(h, W, *, seed: int, step: int, rows=None, bias=None, temperature=None
     return Scores(rows=rows, v_global=v_global, ltilde=lt, g=g, s=s)
 
 
+def scores_from_logits(logits, *, seed: int, step: int, rows=None, bias=None, temperature=None,
+                       mask=None) -> Scores:
+    """O3-O5 on pre-materialised logits l [B, V] (standalone sampling, §5.2 P:490-493 /
+    Alg. A.1): the same transform, RNG layout and perturbation as the fused path."""
+    lg = to_f64(logits)
+    B, V = lg.shape
+    rows = np.arange(B) if rows is None else np.asarray(rows)
+    v_global = np.arange(V, dtype=np.int64)
+    lt, _ = transform(lg[rows], rows, v_global, bias, temperature, mask)
+    g = rng.gumbel_at(seed, step, rows[:, None], v_global[None, :])
+    return Scores(rows=rows, v_global=v_global, ltilde=lt, g=g, s=lt + g)
+
+
+def log_prob(sc: Scores, res: "FlatResult") -> np.ndarray:
+    """log p(idx) = l~_idx - logsumexp(l~)  (App. E P:882: log-normalizer -> log-probabilities);
+    -inf for undefined rows."""
+    out = np.full(len(res.idx), -np.inf)
+    for r, i in enumerate(res.idx):
+        if i >= 0:
+            j = int(np.nonzero(sc.v_global == i)[0][0])
+            out[r] = sc.ltilde[r, j] - res.logZ[r]
+    return out
+
+
 def logsumexp(x, axis=-1) -> np.ndarray:
     """Max-shifted log(sum(exp(x))); -inf for an all -inf (or empty) slice."""
     x = np.asarray(x, dtype=np.float64)

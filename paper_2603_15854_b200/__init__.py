@@ -20,7 +20,7 @@ import torch
 from . import _lib
 from ._lib import FS_BF16, FS_F32, FlashSampleError
 
-__all__ = ["sample", "sample_grouped", "sample_shard", "combine_summaries", "merge_summaries",
+__all__ = ["sample", "sample_grouped", "sample_logits", "sample_shard", "combine_summaries", "merge_summaries",
            "random_bits", "gumbel_from_bits", "Summaries", "context", "set_option", "query",
            "FlashSampleError", "version", "sample_from_host"]
 
@@ -128,20 +128,51 @@ class Summaries:
 
 
 def sample_grouped(h, W, *, group_size: int, bias=None, temperature=None, mask=None, seed: int = 0,
-                   step: int = 0, return_groups: bool = True):
+                   step: int = 0, return_groups: bool = True, return_logprob: bool = False):
     """Grouped FlashSampling (fs_sample_grouped).  Returns (idx [B] int32, score [B] fp32,
-    logZ [B] fp32, Summaries [B, ceil(V/g)] or None)."""
+    logZ [B] fp32, Summaries [B, ceil(V/g)] or None) [+ logprob [B] fp32 if return_logprob]."""
     B, D, V = _check_inputs(h, W, bias, temperature, mask)
     n_groups = (V + group_size - 1) // group_size
     idx = torch.empty(B, dtype=torch.int32, device=h.device)
     score = torch.empty(B, dtype=torch.float32, device=h.device)
     logZ = torch.empty(B, dtype=torch.float32, device=h.device)
+    logprob = torch.empty(B, dtype=torch.float32, device=h.device) if return_logprob else None
     groups = Summaries.empty(B, n_groups, device=h.device) if return_groups else None
     _lib.check(_lib.lib().fs_sample_grouped(
         context(h.device), _dtype_code(h, W), _ptr(h), _ptr(W), _ptr(bias), _ptr(temperature), _ptr(mask),
         seed & (2**64 - 1), step & (2**64 - 1), B, D, V, group_size, _ptr(idx), _ptr(score), _ptr(logZ),
-        _ptr(groups.raw) if groups else None, _stream(h)), "fs_sample_grouped")
+        _ptr(logprob), _ptr(groups.raw) if groups else None, _stream(h)), "fs_sample_grouped")
+    if return_logprob:
+        return idx, score, logZ, groups, logprob
     return idx, score, logZ, groups
+
+
+def sample_logits(logits, *, bias=None, temperature=None, mask=None, seed: int = 0, step: int = 0,
+                  return_all: bool = False):
+    """Standalone Gumbel-max over materialised logits [B, V] (bf16 or fp32, row stride may exceed V)
+    (fs_sample_logits).  Returns idx [B], or (idx, score, logZ, logprob) if return_all."""
+    if not logits.is_cuda or logits.dim() != 2 or logits.stride(1) != 1:
+        raise ValueError("logits must be a 2-D CUDA tensor with unit column stride")
+    B, V = logits.shape
+    if bias is not None and (bias.dtype != torch.float32 or bias.numel() != V):
+        raise ValueError("bias must be fp32 [V]")
+    if temperature is not None and (temperature.dtype != torch.float32 or temperature.numel() != B):
+        raise ValueError("temperature must be fp32 [B]")
+    if mask is not None and (mask.dtype != torch.int32 or tuple(mask.shape) != (B, (V + 31) // 32)):
+        raise ValueError("mask must be int32 [B, ceil(V/32)]")
+    code = FS_BF16 if logits.dtype == torch.bfloat16 else FS_F32 if logits.dtype == torch.float32 else None
+    if code is None:
+        raise TypeError("logits must be bf16 or fp32")
+    dev = logits.device
+    idx = torch.empty(B, dtype=torch.int32, device=dev)
+    score = torch.empty(B, dtype=torch.float32, device=dev) if return_all else None
+    logZ = torch.empty(B, dtype=torch.float32, device=dev) if return_all else None
+    logprob = torch.empty(B, dtype=torch.float32, device=dev) if return_all else None
+    _lib.check(_lib.lib().fs_sample_logits(
+        context(dev), code, _ptr(logits), logits.stride(0), _ptr(bias), _ptr(temperature), _ptr(mask),
+        seed & (2**64 - 1), step & (2**64 - 1), B, V, _ptr(idx), _ptr(score), _ptr(logZ), _ptr(logprob),
+        _stream(logits)), "fs_sample_logits")
+    return (idx, score, logZ, logprob) if return_all else idx
 
 
 def sample_shard(h, W_shard, vocab_offset: int, V_total: int, *, bias_shard=None, temperature=None,

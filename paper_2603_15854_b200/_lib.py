@@ -14,7 +14,7 @@ LIB_PATH = os.path.join(HERE, "libflashsample.so")
 # Every symbol include/flashsample.h declares (checked by tests/test_abi.py).
 EXPORTS = [
     "fs_version", "fs_status_str", "fs_last_error", "fs_ctx_create", "fs_ctx_destroy",
-    "fs_ctx_set_option", "fs_ctx_query", "fs_sample", "fs_sample_grouped", "fs_sample_shard",
+    "fs_ctx_set_option", "fs_ctx_query", "fs_sample", "fs_sample_grouped", "fs_sample_logits", "fs_sample_shard",
     "fs_combine_summaries", "fs_merge_summaries", "fs_random_bits", "fs_gumbel_from_bits",
 ]
 
@@ -52,7 +52,8 @@ def lib() -> ctypes.CDLL:
     L.fs_ctx_query.argtypes = [vp, ctypes.c_char_p, ctypes.POINTER(ctypes.c_double)]
     L.fs_sample.argtypes = [vp, i32, vp, vp, vp, vp, vp, u64, u64, i32, i32, i32, vp, vp, vp]
     L.fs_sample_grouped.argtypes = [vp, i32, vp, vp, vp, vp, vp, u64, u64, i32, i32, i32, i32,
-                                    vp, vp, vp, vp, vp]
+                                    vp, vp, vp, vp, vp, vp]
+    L.fs_sample_logits.argtypes = [vp, i32, vp, i64, vp, vp, vp, u64, u64, i32, i32, vp, vp, vp, vp, vp]
     L.fs_sample_shard.argtypes = [vp, i32, vp, vp, vp, vp, vp, u64, u64, i32, i32, i32, i64, i64, vp, vp]
     L.fs_combine_summaries.argtypes = [vp, i32, i32, vp, vp, vp, vp]
     L.fs_merge_summaries.argtypes = [vp, vp, vp, i32, vp]

@@ -177,6 +177,7 @@ struct PathArgs {
   float* logZ_out;
   fs_summary* groups_out;
   int n_groups;
+  float* logprob_out;
 };
 
 fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
@@ -279,7 +280,7 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
     e = fs::launch_reduce(part, part_group, lay, Bc, a.n_groups, a.idx_out ? a.idx_out + r0 : nullptr,
                           a.score_out ? a.score_out + r0 : nullptr, a.logZ_out ? a.logZ_out + r0 : nullptr,
                           a.groups_out ? a.groups_out + (size_t)r0 * a.n_groups : nullptr, stream,
-                          ctx->pdl != 0 && !ctx->time_stage1);
+                          ctx->pdl != 0 && !ctx->time_stage1, a.logprob_out ? a.logprob_out + r0 : nullptr);
     if (e != cudaSuccess) return cuda_fail(e, "stage-2 reduce launch");
   }
   return FS_OK;
@@ -410,21 +411,21 @@ fs_status fs_sample(fs_ctx* ctx, fs_dtype dtype, const void* h, const void* W, c
   if (s != FS_OK) return s;
   if (!idx_out) return fail(FS_ERR_INVALID, "idx_out is required");
   PathArgs a{dtype, h, W, bias, temperature, mask, ((int64_t)V + 31) / 32, seed, step, B, D, V, 0,
-             ((V + 127) / 128) * 128, false, idx_out, score_out, nullptr, nullptr, 1};
+             ((V + 127) / 128) * 128, false, idx_out, score_out, nullptr, nullptr, 1, nullptr};
   return run_path(ctx, a, static_cast<cudaStream_t>(stream));
 }
 
 fs_status fs_sample_grouped(fs_ctx* ctx, fs_dtype dtype, const void* h, const void* W, const float* bias,
                             const float* temperature, const uint32_t* mask, uint64_t seed, uint64_t step, int B,
                             int D, int V, int group_size, int32_t* idx_out, float* score_out, float* logZ_out,
-                            fs_summary* groups_out, void* stream) {
+                            float* logprob_out, fs_summary* groups_out, void* stream) {
   fs_status s = check_common(ctx, dtype, h, W, B, D, V);
   if (s != FS_OK) return s;
   if (!idx_out) return fail(FS_ERR_INVALID, "idx_out is required");
   if (group_size < 128 || group_size % 128 != 0) return fail(FS_ERR_INVALID, "group_size must be a positive multiple of 128");
   const int n_groups = (V + group_size - 1) / group_size;
   PathArgs a{dtype, h, W, bias, temperature, mask, ((int64_t)V + 31) / 32, seed, step, B, D, V, 0,
-             group_size, true, idx_out, score_out, logZ_out, groups_out, n_groups};
+             group_size, true, idx_out, score_out, logZ_out, groups_out, n_groups, logprob_out};
   return run_path(ctx, a, static_cast<cudaStream_t>(stream));
 }
 
@@ -437,8 +438,36 @@ fs_status fs_sample_shard(fs_ctx* ctx, fs_dtype dtype, const void* h, const void
   if (vocab_offset < 0 || V_total < vocab_offset + V_local || V_total >= (1LL << 31))
     return fail(FS_ERR_INVALID, "need 0 <= vocab_offset, vocab_offset + V_local <= V_total < 2^31");
   PathArgs a{dtype, h, W_shard, bias_shard, temperature, mask, (V_total + 31) / 32, seed, step, B, D, V_local,
-             vocab_offset, ((V_local + 127) / 128) * 128, true, nullptr, nullptr, nullptr, summary_out, 1};
+             vocab_offset, ((V_local + 127) / 128) * 128, true, nullptr, nullptr, nullptr, summary_out, 1, nullptr};
   return run_path(ctx, a, static_cast<cudaStream_t>(stream));
+}
+
+fs_status fs_sample_logits(fs_ctx* ctx, fs_dtype dtype, const void* logits, int64_t ld, const float* bias,
+                           const float* temperature, const uint32_t* mask, uint64_t seed, uint64_t step, int B, int V,
+                           int32_t* idx_out, float* score_out, float* logZ_out, float* logprob_out, void* stream) {
+  if (!ctx) return fail(FS_ERR_INVALID, "ctx is NULL");
+  if (dtype != FS_BF16 && dtype != FS_F32) return fail(FS_ERR_INVALID, "unknown dtype");
+  if (!logits || !idx_out) return fail(FS_ERR_INVALID, "logits and idx_out are required");
+  if (B < 1 || V < 1 || ld < V) return fail(FS_ERR_INVALID, "need B >= 1, V >= 1, ld >= V");
+  if (B > 65535 * 4) return fail(FS_ERR_UNSUPPORTED, "B too large");
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  cudaStream_t stream_ = static_cast<cudaStream_t>(stream);
+  const int nblk = fs::logits_sample_blocks(B, V);
+  const size_t part_bytes = (size_t)nblk * B * sizeof(fs::State);
+  const size_t grp_off = (part_bytes + 255) & ~size_t(255);
+  fs_status st = ensure_ws(ctx, grp_off + (size_t)nblk * sizeof(int));
+  if (st != FS_OK) return st;
+  fs::State* part = static_cast<fs::State*>(ctx->ws);
+  int* part_group = reinterpret_cast<int*>(static_cast<char*>(ctx->ws) + grp_off);
+  const bool lse = logZ_out || logprob_out;
+  e = fs::launch_logits_sample(dtype, logits, ld, bias, temperature, mask, ((int64_t)V + 31) / 32, B, V, seed, step,
+                               lse, nblk, part, part_group, stream_);
+  if (e != cudaSuccess) return cuda_fail(e, "logits sampler launch");
+  const fs::SlotLayout lay{nblk, 1, nblk, V, 1, V, 128, 0};
+  e = fs::launch_reduce(part, part_group, lay, B, 1, idx_out, score_out, logZ_out, nullptr, stream_, ctx->pdl != 0,
+                        logprob_out);
+  return e == cudaSuccess ? FS_OK : cuda_fail(e, "stage-2 reduce launch");
 }
 
 fs_status fs_combine_summaries(const fs_summary* gathered, int n, int B, int32_t* idx_out, float* score_out,

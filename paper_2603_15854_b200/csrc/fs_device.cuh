@@ -107,13 +107,14 @@ __device__ __forceinline__ float key_to_float(uint32_t k) {
 constexpr uint32_t kKeyNegInf = 0x007FFFFFu;
 constexpr uint32_t kKeyNone = 0u;
 
-// Running state of a (row, vocabulary range): best key, its smallest global id, and the
-// log-mass S = sum exp(l~ - M) relative to M = key_to_float(key) (App. E).
+// Running state of a (row, vocabulary range): best key, its smallest global id, the log-mass
+// S = sum exp(l~ - M) relative to M = key_to_float(key) (App. E), and the transformed
+// logit l~ of the best element (float bits; gives log p(idx) = l~_idx - logZ).
 struct State {
   uint32_t key;
   int32_t idx;
   float S;
-  uint32_t pad;
+  uint32_t lt;
 };
 
 __device__ __forceinline__ State state_empty() { return State{kKeyNone, -1, 0.0f, 0u}; }

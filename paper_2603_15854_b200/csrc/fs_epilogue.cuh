@@ -39,11 +39,12 @@ struct RowArgs {
 // warp in increasing vocabulary order, so a strictly larger key wins and an equal key keeps
 // the earlier (smaller) id.
 template <bool LSE>
-__device__ __forceinline__ void absorb(State& own, uint32_t kmax, int32_t widx, float S_w) {
+__device__ __forceinline__ void absorb(State& own, uint32_t kmax, int32_t widx, float S_w, float ltw = 0.0f) {
   if (kmax > own.key) {
     if (LSE) {
       const float m_old = key_ref(own.key), m_new = key_ref(kmax);
       own.S = (own.key > kKeyNegInf ? own.S * fast_exp2((m_old - m_new) * kLog2e) : 0.0f) + S_w;
+      own.lt = __float_as_uint(ltw);
     }
     own.key = kmax;
     own.idx = widx;
@@ -85,7 +86,8 @@ __device__ __forceinline__ void epi_columns(const float* acc, int col0, const Ro
         for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xFFFFFFFFu, e, o);
         S_w = e;
       }
-      if (lane == ((j + jj) & 31)) absorb<LSE>(own, kmax, widx, S_w);
+      const float ltw = LSE ? __shfl_sync(0xFFFFFFFFu, lt, kmax > kKeyNone ? __ffs(ball) - 1 : 0) : 0.0f;
+      if (lane == ((j + jj) & 31)) absorb<LSE>(own, kmax, widx, S_w, ltw);
     }
   }
 }
@@ -253,7 +255,13 @@ __device__ __forceinline__ void epi_tile_tc(uint32_t taddr, const RowArgs& ra, c
           if (o <= bit) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
         constexpr int kShift = (NC == 16) ? 1 : 2;          // column of lane L = L >> kShift
         const float Sw = __shfl_sync(0xFFFFFFFFu, v, (jo & (NC - 1)) << kShift);
-        if (mine) absorb<true>(own, km, wi, Sw);
+        float ltw = 0.0f;                                    // l~ of each column's winner
+#pragma unroll
+        for (int jj = 0; jj < NC; ++jj) {
+          const float x = __shfl_sync(0xFFFFFFFFu, lt[jj], kmax[jj] > kKeyNone ? __ffs(ball[jj]) - 1 : 0);
+          ltw = (jo == jj) ? x : ltw;
+        }
+        if (mine) absorb<true>(own, km, wi, Sw, ltw);
       } else {
         const bool upd = mine && (km > own.key);       // ties keep the earlier (smaller) id
         own.key = upd ? km : own.key;

@@ -66,7 +66,13 @@ struct SlotLayout {
 // Stage 2: reduce the candidate slots of every row into groups and the final sample.
 cudaError_t launch_reduce(const State* part, const int* part_group, const SlotLayout& lay, int B, int n_groups,
                           int32_t* idx_out, float* score_out, float* logZ_out, fs_summary* groups_out,
-                          cudaStream_t stream, bool pdl);
+                          cudaStream_t stream, bool pdl, float* logprob_out = nullptr);
+// Standalone sampler over materialised logits [B][ld] (bf16 or fp32): candidates per (V-block, row).
+cudaError_t launch_logits_sample(fs_dtype dtype, const void* logits, int64_t ld, const float* bias,
+                                 const float* temperature, const uint32_t* mask, int64_t mask_words, int B, int V,
+                                 uint64_t seed, uint64_t step, bool lse, int nblk, State* part, int* part_group,
+                                 cudaStream_t stream);
+int logits_sample_blocks(int B, int V);   // V blocks of the standalone sampler grid
 cudaError_t launch_combine(const fs_summary* gathered, int n, int B, int32_t* idx_out, float* score_out,
                            float* logZ_out, cudaStream_t stream);
 cudaError_t launch_merge(const fs_summary* a, const fs_summary* b, fs_summary* out, int count,

@@ -1,0 +1,147 @@
+// fs_logits.cu -- standalone FlashSampling over materialised logits.
+//
+// Gumbel-max over a [B, V] logits matrix that some other kernel already wrote (§5.2
+// P:490-493, Alg. A.1 P:747-763 parallelised like Alg. 2): same transform, RNG layout, tie rule
+// and candidate format as the fused path, so fs_sample_logits(h W^T) == fs_sample(h, W) up to the
+// fp32 rounding of the logits.  Optionally the log-normalizer and log p(idx) (App. E).
+//
+// HBM-bound (reads B*V*esz bytes once).  Grid (V blocks) x (B/4): a thread owns one vocabulary
+// column v and 4 rows b0..b0+3, so one Philox call serves 4 rows (the counter layout's b>>2) and
+// the 4 row reads are each coalesced along v.  Candidates: one per (V block, row).
+#include <cuda_bf16.h>
+
+#include <algorithm>
+
+#include "fs_device.cuh"
+#include "fs_sm100.cuh"
+#include "fs_kernels.h"
+
+namespace fs {
+
+namespace {
+
+template <typename T>
+__device__ __forceinline__ float ld_logit(const T* p) {
+  if constexpr (sizeof(T) == 2) return __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(p));
+  else return *p;
+}
+
+__device__ __forceinline__ State shfl_state(const State& a, int o) {
+  State r;
+  r.key = __shfl_xor_sync(0xFFFFFFFFu, a.key, o);
+  r.idx = __shfl_xor_sync(0xFFFFFFFFu, a.idx, o);
+  r.S = __shfl_xor_sync(0xFFFFFFFFu, a.S, o);
+  r.lt = __shfl_xor_sync(0xFFFFFFFFu, a.lt, o);
+  return r;
+}
+
+template <typename T, bool XFORM, bool LSE>
+__global__ void __launch_bounds__(256)
+logits_sample_kernel(const T* __restrict__ logits, int64_t ld, const float* __restrict__ bias,
+                     const float* __restrict__ temperature, const uint32_t* __restrict__ mask, int64_t mask_words,
+                     int B, int V, int vpb, uint32_t k0, uint32_t k1, uint32_t c2, uint32_t c3, State* part,
+                     int* part_group) {
+  __shared__ State red[8][4];
+  const int b0 = blockIdx.y * 4;
+  const int v_begin = blockIdx.x * vpb, v_end = min(V, v_begin + vpb);
+  float it[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int b = b0 + j;
+    it[j] = __int_as_float(0x7FC00000);
+    if (b < B) {
+      const float t = (XFORM && temperature) ? temperature[b] : 1.0f;
+      if (t > 0.0f && isfinite(t)) it[j] = 1.0f / t;
+    }
+  }
+  State st[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) st[j] = state_empty();
+  for (int v = v_begin + (int)threadIdx.x; v < v_end; v += 256) {
+    const U4 r4 = philox4x32_10((uint32_t)v, (uint32_t)b0 >> 2, c2, c3, k0, k1);
+    const uint32_t rr[4] = {r4.x, r4.y, r4.z, r4.w};
+    const float bv = (XFORM && bias) ? bias[v] : 0.0f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int b = b0 + j;
+      if (b >= B) break;                                     // block-uniform
+      float l = ld_logit(logits + (int64_t)b * ld + v);
+      if (XFORM) {
+        l = (l + bv) * it[j];
+        if (mask && !((mask[(int64_t)b * mask_words + (v >> 5)] >> (v & 31)) & 1u)) l = -INFINITY;
+      }
+      if (isnan(l)) l = -INFINITY;
+      const float s = l + gumbel32(rr[j]);
+      const uint32_t key = order_key(s);
+      if (key > st[j].key) {                                 // v ascends per thread: ties keep smaller v
+        if (LSE) {
+          st[j].S = (st[j].key > kKeyNegInf ? st[j].S * fast_exp2((key_ref(st[j].key) - s) * kLog2e) : 0.0f) +
+                    (s != -INFINITY ? fast_exp2((l - s) * kLog2e) : 0.0f);
+          st[j].lt = __float_as_uint(l);
+        }
+        st[j].key = key;
+        st[j].idx = v;
+      } else if (LSE && st[j].key > kKeyNegInf) {
+        st[j].S += fast_exp2((l - key_ref(st[j].key)) * kLog2e);
+      }
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    State x = st[j];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const State y = shfl_state(x, o);
+      x = (lane & o) ? state_merge(y, x) : state_merge(x, y);
+    }
+    if (lane == 0) red[warp][j] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    const int j = threadIdx.x, b = b0 + j;
+    State x = red[0][j];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) x = state_merge(x, red[w][j]);
+    if (b < B) part[(size_t)blockIdx.x * B + b] = x;
+  }
+  if (threadIdx.x == 0 && blockIdx.y == 0) part_group[blockIdx.x] = 0;
+  sm100::pdl_launch_dependents();
+}
+
+}  // namespace
+
+cudaError_t launch_logits_sample(fs_dtype dtype, const void* logits, int64_t ld, const float* bias,
+                                 const float* temperature, const uint32_t* mask, int64_t mask_words, int B, int V,
+                                 uint64_t seed, uint64_t step, bool lse, int nblk, State* part, int* part_group,
+                                 cudaStream_t stream) {
+  const int vpb = ((V + nblk - 1) / nblk + 255) / 256 * 256;
+  const dim3 grid((V + vpb - 1) / vpb, (B + 3) / 4);
+  const bool xform = bias || temperature || mask;
+  const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  const uint32_t c2 = (uint32_t)step, c3 = (uint32_t)(step >> 32) & 0x00FFFFFFu;
+#define FS_LAUNCH(T, X, L)                                                                                   \
+  logits_sample_kernel<T, X, L><<<grid, 256, 0, stream>>>(static_cast<const T*>(logits), ld, bias, temperature, \
+                                                          mask, mask_words, B, V, vpb, k0, k1, c2, c3, part,  \
+                                                          part_group)
+  if (dtype == FS_BF16) {
+    if (xform) { if (lse) FS_LAUNCH(uint16_t, true, true); else FS_LAUNCH(uint16_t, true, false); }
+    else       { if (lse) FS_LAUNCH(uint16_t, false, true); else FS_LAUNCH(uint16_t, false, false); }
+  } else {
+    if (xform) { if (lse) FS_LAUNCH(float, true, true); else FS_LAUNCH(float, true, false); }
+    else       { if (lse) FS_LAUNCH(float, false, true); else FS_LAUNCH(float, false, false); }
+  }
+#undef FS_LAUNCH
+  return cudaGetLastError();
+}
+
+int logits_sample_blocks(int B, int V) {
+  // >= 2 waves of 148 SMs over (V blocks) x (B/4), at least 256 columns per block
+  const int rows4 = (B + 3) / 4;
+  int nblk = (2 * 148 + rows4 - 1) / rows4;
+  nblk = std::max(1, std::min(nblk, (V + 255) / 256));
+  const int vpb = ((V + nblk - 1) / nblk + 255) / 256 * 256;
+  return (V + vpb - 1) / vpb;
+}
+
+}  // namespace fs

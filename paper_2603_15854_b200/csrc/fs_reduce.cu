@@ -36,12 +36,19 @@ __device__ __forceinline__ State from_summary(const fs_summary& m) {
 
 constexpr int kReduceThreads = 256;
 
+// log p(idx) = l~_idx - logZ (App. E); -inf when the row is undefined.
+__device__ __forceinline__ float logprob_of(const State& s) {
+  const fs_summary f = to_summary(s);
+  return f.idx >= 0 && f.log_mass > -INFINITY ? __uint_as_float(s.lt) - f.log_mass : -INFINITY;
+}
+
 // Single group (Alg. 2 stage 2; or one TP shard's summary): one warp per batch row,
 // each lane merges slots lane, lane+32, ... (independent loads in flight), then a fixed
 // shuffle tree -- deterministic, so logZ is bit-reproducible.
 __global__ void __launch_bounds__(128)
 reduce_rows_kernel(const State* __restrict__ part, const int* __restrict__ part_group, int n_slots, int B,
-                   int32_t* idx_out, float* score_out, float* logZ_out, fs_summary* groups_out) {
+                   int32_t* idx_out, float* score_out, float* logZ_out, fs_summary* groups_out,
+                   float* logprob_out) {
   sm100::pdl_wait();                       // stage-1 results are visible past this point
   const int lane = threadIdx.x & 31;
   const int b = blockIdx.x * 4 + (threadIdx.x >> 5);
@@ -56,7 +63,7 @@ reduce_rows_kernel(const State* __restrict__ part, const int* __restrict__ part_
     other.key = __shfl_xor_sync(0xFFFFFFFFu, acc.key, o);
     other.idx = __shfl_xor_sync(0xFFFFFFFFu, acc.idx, o);
     other.S = __shfl_xor_sync(0xFFFFFFFFu, acc.S, o);
-    other.pad = 0u;
+    other.lt = __shfl_xor_sync(0xFFFFFFFFu, acc.lt, o);
     acc = (lane & o) ? state_merge(other, acc) : state_merge(acc, other);
   }
   if (lane == 0) {
@@ -65,6 +72,7 @@ reduce_rows_kernel(const State* __restrict__ part, const int* __restrict__ part_
     if (score_out) score_out[b] = f.max_score;
     if (logZ_out) logZ_out[b] = f.log_mass;
     if (groups_out) groups_out[b] = f;
+    if (logprob_out) logprob_out[b] = logprob_of(acc);
   }
 }
 
@@ -86,13 +94,14 @@ __device__ __forceinline__ State shfl_xor_state(const State& a, int o) {
   r.key = __shfl_xor_sync(0xFFFFFFFFu, a.key, o);
   r.idx = __shfl_xor_sync(0xFFFFFFFFu, a.idx, o);
   r.S = __shfl_xor_sync(0xFFFFFFFFu, a.S, o);
-  r.pad = 0u;
+  r.lt = __shfl_xor_sync(0xFFFFFFFFu, a.lt, o);
   return r;
 }
 
 __global__ void __launch_bounds__(kReduceThreads)
 reduce_groups_kernel(const State* __restrict__ part, const int* __restrict__ part_group, int n_slots, int B,
-                     int n_groups, int32_t* idx_out, float* score_out, float* logZ_out, fs_summary* groups_out) {
+                     int n_groups, int32_t* idx_out, float* score_out, float* logZ_out, fs_summary* groups_out,
+                     float* logprob_out) {
   extern __shared__ int sg[];
   __shared__ State red[kReduceThreads];
   sm100::pdl_wait();
@@ -139,6 +148,7 @@ reduce_groups_kernel(const State* __restrict__ part, const int* __restrict__ par
     if (idx_out) idx_out[b] = f.idx;
     if (score_out) score_out[b] = f.max_score;
     if (logZ_out) logZ_out[b] = f.log_mass;
+    if (logprob_out) logprob_out[b] = logprob_of(red[0]);
   }
 }
 
@@ -179,7 +189,7 @@ __global__ void gumbel_kernel(const uint32_t* r, float* g, int64_t n) {
 
 cudaError_t launch_reduce(const State* part, const int* part_group, const SlotLayout& lay, int B, int n_groups,
                           int32_t* idx_out, float* score_out, float* logZ_out, fs_summary* groups_out,
-                          cudaStream_t stream, bool pdl) {
+                          cudaStream_t stream, bool pdl, float* logprob_out) {
   cudaLaunchConfig_t cfg = {};
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -191,7 +201,7 @@ cudaError_t launch_reduce(const State* part, const int* part_group, const SlotLa
     cfg.gridDim = dim3((B + 3) / 4);
     cfg.blockDim = dim3(128);
     return cudaLaunchKernelEx(&cfg, reduce_rows_kernel, part, part_group, lay.n_slots, B, idx_out, score_out,
-                              logZ_out, groups_out);
+                              logZ_out, groups_out, logprob_out);
   }
   cfg.gridDim = dim3(B);
   cfg.blockDim = dim3(kReduceThreads);
@@ -202,7 +212,7 @@ cudaError_t launch_reduce(const State* part, const int* part_group, const SlotLa
     if (e != cudaSuccess) return e;
   }
   return cudaLaunchKernelEx(&cfg, reduce_groups_kernel, part, part_group, lay.n_slots, B, n_groups, idx_out,
-                            score_out, logZ_out, groups_out);
+                            score_out, logZ_out, groups_out, logprob_out);
 }
 
 cudaError_t launch_combine(const fs_summary* gathered, int n, int B, int32_t* idx_out, float* score_out,

@@ -234,3 +234,24 @@ def test_chi_square_statistic_spec_example():
     stat, p = stats.chi_square([30, 70], [0.5, 0.5])
     assert stat == pytest.approx(16.0)
     assert p == pytest.approx(6.334e-5, rel=1e-3)
+
+
+def test_scores_from_logits_equal_fused_definition():
+    # standalone sampling on materialised logits l = h W^T gives the fused path's sample
+    rs = np.random.default_rng(21)
+    h = rs.standard_normal((5, 12)).astype(np.float32)
+    W = rs.standard_normal((300, 12)).astype(np.float32)
+    logits = sampler.logits(h, W)
+    a = sampler.flat_sample(sampler.scores(h, W, seed=3, step=9))
+    b = sampler.flat_sample(sampler.scores_from_logits(logits, seed=3, step=9))
+    assert np.array_equal(a.idx, b.idx)
+    np.testing.assert_allclose(a.s1, b.s1, rtol=0, atol=1e-12)
+
+
+def test_log_prob_closed_form():
+    # l~ = [ln 1, ln 2, ln 3, ln 4] -> p = [.1, .2, .3, .4]; log p(idx) must be log(p[idx])
+    lt = np.log(np.array([[1.0, 2.0, 3.0, 4.0]] * 64))
+    sc = sampler.scores_from_logits(lt, seed=5, step=0)
+    res = sampler.flat_sample(sc)
+    lp = sampler.log_prob(sc, res)
+    np.testing.assert_allclose(lp, np.log([0.1, 0.2, 0.3, 0.4])[res.idx], rtol=0, atol=1e-12)

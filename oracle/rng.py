@@ -66,6 +66,28 @@ def random_bits(seed: int, step: int, b, v, tag: int = TAG_TOKEN) -> np.ndarray:
     return np.take_along_axis(stacked, lane[None], axis=0)[0]
 
 
+# Per-request layout (reading R18): batch-position-invariant noise.
+#   key = (seed_b mod 2^32, seed_b >> 32)
+#   ctr = (v >> 2, 0x80000000, step_b mod 2^32, ((step_b >> 32) mod 2^24) | (tag << 24))
+#   r   = Philox4x32-10(ctr, key)[v mod 4]
+# Word 1 = 0x80000000 never equals b >> 2 of the shared layout for B < 2^33, so the two layouts
+# draw from disjoint counters.
+PER_REQUEST_WORD1 = 0x80000000
+
+
+def random_bits_per_request(seeds, steps, v, tag: int = TAG_TOKEN) -> np.ndarray:
+    """r for (request seed_b, step_b, vocabulary id v); seeds/steps/v broadcast (uint64)."""
+    seeds = np.asarray(seeds).astype(np.uint64)
+    v = np.asarray(v, dtype=np.uint64)
+    c2, c3 = counter_words(steps, tag)
+    seeds, v, c2, c3 = np.broadcast_arrays(seeds, v, c2, c3)
+    k0 = seeds & np.uint64(0xFFFFFFFF)
+    k1 = seeds >> np.uint64(32)
+    o = philox4x32(v >> np.uint64(2), np.full(v.shape, PER_REQUEST_WORD1, np.uint64), c2, c3, k0, k1)
+    lane = (v & np.uint64(3)).astype(np.int64)
+    return np.take_along_axis(np.stack(o, axis=0), lane[None], axis=0)[0]
+
+
 def uniform_open(r) -> np.ndarray:
     """u = (r+1)/(2^32+1) in fp64 (App. C)."""
     return (np.asarray(r, dtype=np.float64) + 1.0) / DEN

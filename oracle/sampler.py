@@ -57,16 +57,26 @@ def allowed_bits(mask, rows, v_global) -> np.ndarray:
     return ((w >> (v_global % 32).astype(np.uint32)) & np.uint32(1)).astype(bool)
 
 
+def greedy_rows(temperature, rows):
+    """Rows sampled greedily: tau == 0 exactly (reading R18; "greedy ... would
+    disable FlashSampling" -- greedy is argmax without noise)."""
+    if temperature is None:
+        return np.zeros(len(np.atleast_1d(rows)), dtype=bool)
+    return np.asarray(temperature, dtype=np.float64)[np.asarray(rows)] == 0.0
+
+
 def transform(ell, rows, v_global, bias=None, temperature=None, mask=None):
-    """O3: l~ = (l + bias_v)/tau_b, banned or NaN -> -inf.  Returns (l~, row_valid)."""
+    """O3: l~ = (l + bias_v)/tau_b, banned or NaN -> -inf.  Returns (l~, row_valid).
+    tau == 0: greedy row, l~ = l + bias_v (no scaling); tau < 0 or non-finite: undefined row."""
     lt = ell.copy()
     if bias is not None:
         lt = lt + np.asarray(bias, dtype=np.float64)[None, :]
     row_valid = np.ones(lt.shape[0], dtype=bool)
     if temperature is not None:
         tau = np.asarray(temperature, dtype=np.float64)[np.asarray(rows)]
-        row_valid = np.isfinite(tau) & (tau > 0)
-        safe = np.where(row_valid, tau, 1.0)
+        greedy = tau == 0.0
+        row_valid = np.isfinite(tau) & (tau >= 0)
+        safe = np.where(row_valid & ~greedy, tau, 1.0)
         lt = lt / safe[:, None]
     if mask is not None:
         lt = np.where(allowed_bits(mask, rows, v_global), lt, -np.inf)
@@ -84,8 +94,23 @@ class Scores:
     s: np.ndarray             # [R, Vl] perturbed scores (fp64)
 
 
+def noise(seed, step, rows, v_global, seeds=None, steps=None, temperature=None) -> np.ndarray:
+    """O4: Gumbel noise [R, V]: shared layout (R1) or per-request layout (R18) when `seeds`
+    ([B] uint64) is given (`steps` [B] or None -> the scalar step); 0 on greedy rows."""
+    rows = np.asarray(rows)
+    if seeds is None:
+        g = rng.gumbel_at(seed, step, rows[:, None], v_global[None, :])
+    else:
+        sd = np.asarray(seeds).astype(np.uint64)[rows]
+        stp = (np.full(len(rows), int(step) & 0xFFFFFFFFFFFFFFFF, np.uint64) if steps is None
+               else np.asarray(steps).astype(np.uint64)[rows])
+        g = rng.gumbel64(rng.random_bits_per_request(sd[:, None], stp[:, None], v_global[None, :]))
+    g = np.where(greedy_rows(temperature, rows)[:, None], 0.0, g)
+    return g
+
+
 def scores(h, W, *, seed: int, step: int, rows=None, bias=None, temperature=None,
-           mask=None, vocab_offset: int = 0) -> Scores:
+           mask=None, vocab_offset: int = 0, seeds=None, steps=None) -> Scores:
     """O1-O5 for the selected rows.  W (and bias) may be a vocabulary shard whose first
     row has global id `vocab_offset`; the RNG and the mask are keyed by global ids."""
     B = np.asarray(h).shape[0]
@@ -94,13 +119,13 @@ def scores(h, W, *, seed: int, step: int, rows=None, bias=None, temperature=None
     v_global = np.arange(vocab_offset, vocab_offset + V_local, dtype=np.int64)
     ell = logits(h, W, rows)
     lt, _ = transform(ell, rows, v_global, bias, temperature, mask)
-    g = rng.gumbel_at(seed, step, rows[:, None], v_global[None, :])
+    g = noise(seed, step, rows, v_global, seeds, steps, temperature)
     s = lt + g                      # -inf + finite = -inf
     return Scores(rows=rows, v_global=v_global, ltilde=lt, g=g, s=s)
 
 
 def scores_from_logits(logits, *, seed: int, step: int, rows=None, bias=None, temperature=None,
-                       mask=None) -> Scores:
+                       mask=None, seeds=None, steps=None) -> Scores:
     """O3-O5 on pre-materialised logits l [B, V] (standalone sampling, §5.2 P:490-493 /
     Alg. A.1): the same transform, RNG layout and perturbation as the fused path."""
     lg = to_f64(logits)
@@ -108,7 +133,7 @@ def scores_from_logits(logits, *, seed: int, step: int, rows=None, bias=None, te
     rows = np.arange(B) if rows is None else np.asarray(rows)
     v_global = np.arange(V, dtype=np.int64)
     lt, _ = transform(lg[rows], rows, v_global, bias, temperature, mask)
-    g = rng.gumbel_at(seed, step, rows[:, None], v_global[None, :])
+    g = noise(seed, step, rows, v_global, seeds, steps, temperature)
     return Scores(rows=rows, v_global=v_global, ltilde=lt, g=g, s=lt + g)
 
 

@@ -19,7 +19,7 @@ import numpy as np
 import pytest
 from scipy.special import logsumexp as sp_lse
 
-from oracle import philox, sampler, stats
+from oracle import philox, rng, sampler, stats
 
 
 def _direct(lt_row_targets, B):
@@ -54,8 +54,11 @@ def test_transform_order_and_mask():
     assert lt[1].tolist() == [-np.inf, 1.0, 2.0]        # banned, 2/2, 4/2
     assert valid.all()
     lt, valid = sampler.transform(ell, np.arange(2), np.arange(3), None,
-                                  np.array([0.0, np.nan], np.float32), None)
+                                  np.array([-1.0, np.nan], np.float32), None)
     assert not valid.any() and np.all(np.isneginf(lt))
+    # tau == 0: greedy row, l~ = l + bias unscaled (reading R18)
+    lt, valid = sampler.transform(ell, np.arange(2), np.arange(3), bias, np.array([0.0, 1.0], np.float32), None)
+    assert valid.all() and lt[0].tolist() == [2.0, 2.0, 4.0]
     # NaN logits are never selectable
     lt, _ = sampler.transform(np.array([[np.nan, 1.0]]), np.arange(1), np.arange(2))
     assert lt[0, 0] == -np.inf
@@ -154,13 +157,13 @@ def test_degenerate_cases():
     # V = 1 -> 0
     h, W = _direct([0.3], 3)
     assert sampler.flat_sample(sampler.scores(h, W, seed=1, step=0)).idx.tolist() == [0, 0, 0]
-    # all masked but j -> j ; all masked -> -1 ; tau <= 0 -> -1
+    # all masked but j -> j ; all masked -> -1 ; tau < 0 -> -1
     h, W = _direct(np.linspace(-3, 3, 40), 4)
     mask = np.zeros((4, 2), np.uint32)
     mask[0, 1] = 1 << (37 - 32)
     mask[2, :] = 0xFFFFFFFF
     mask[3, :] = 0xFFFFFFFF
-    tau = np.array([1, 1, 1, 0], np.float32)
+    tau = np.array([1, 1, 1, -1], np.float32)
     res = sampler.flat_sample(sampler.scores(h, W, seed=1, step=0, mask=mask, temperature=tau))
     assert res.idx[0] == 37 and res.idx[1] == -1 and res.idx[2] >= 0 and res.idx[3] == -1
     assert res.s1[1] == -np.inf and res.logZ[1] == -np.inf
@@ -255,3 +258,51 @@ def test_log_prob_closed_form():
     res = sampler.flat_sample(sc)
     lp = sampler.log_prob(sc, res)
     np.testing.assert_allclose(lp, np.log([0.1, 0.2, 0.3, 0.4])[res.idx], rtol=0, atol=1e-12)
+
+
+def test_greedy_rows_reduce_to_argmax():
+    # tau == 0: no noise, idx = first argmax of l + bias (textbook argmax), for any seed/step
+    rs = np.random.default_rng(8)
+    h = rs.standard_normal((6, 10)).astype(np.float32)
+    W = rs.standard_normal((500, 10)).astype(np.float32)
+    bias = rs.standard_normal(500).astype(np.float32)
+    tau = np.array([0, 0.7, 0, 1.0, 0, 0], np.float32)
+    res = sampler.flat_sample(sampler.scores(h, W, seed=1, step=2, bias=bias, temperature=tau))
+    res2 = sampler.flat_sample(sampler.scores(h, W, seed=99, step=7, bias=bias, temperature=tau))
+    ref = np.argmax(h.astype(np.float64) @ W.astype(np.float64).T + bias, axis=1)
+    for r in np.nonzero(tau == 0)[0]:
+        assert res.idx[r] == ref[r] == res2.idx[r]
+        assert res.s1[r] == (h[r].astype(np.float64) @ W[ref[r]].astype(np.float64) + bias[ref[r]])
+
+
+def test_per_request_layout_explicit_and_position_invariant():
+    seeds = np.array([11, 2**63 + 5, 11, 7], np.uint64)
+    steps = np.array([0, 3, 9, (4 << 32) | 1], np.uint64)
+    v = np.array([0, 1, 2, 3, 4, 1000, 128255])
+    r = rng.random_bits_per_request(seeds[:, None], steps[:, None], v[None, :])
+    for i in range(4):
+        for j, vv in enumerate(v):
+            sd, st = int(seeds[i]), int(steps[i])
+            o = philox.philox4x32(vv >> 2, 0x80000000, st & 0xFFFFFFFF, (st >> 32) & 0xFFFFFF,
+                                  sd & 0xFFFFFFFF, sd >> 32)
+            assert int(r[i, j]) == int(o[vv & 3])
+    # batch-position invariance: permuting rows together with their seeds permutes the samples
+    rs = np.random.default_rng(4)
+    h = rs.standard_normal((5, 8)).astype(np.float32)
+    W = rs.standard_normal((300, 8)).astype(np.float32)
+    sd = np.array([1, 2, 3, 4, 5], np.uint64)
+    perm = np.array([3, 0, 4, 1, 2])
+    a = sampler.flat_sample(sampler.scores(h, W, seed=0, step=6, seeds=sd))
+    b = sampler.flat_sample(sampler.scores(h[perm], W, seed=0, step=6, seeds=sd[perm]))
+    assert np.array_equal(a.idx[perm], b.idx)
+
+
+def test_per_request_chi_square():
+    lt = np.linspace(-1, 2, 8).astype(np.float32)
+    n = 50_000
+    h = np.tile(lt, (n, 1))
+    seeds = np.arange(n, dtype=np.uint64) * np.uint64(2654435761)
+    idx = sampler.flat_sample(sampler.scores(h, np.eye(8, dtype=np.float32), seed=0, step=3, seeds=seeds),
+                              want_near=False).idx
+    _, p = stats.chi_square(np.bincount(idx, minlength=8), stats.softmax_probs(lt))
+    assert p > 1e-3

@@ -404,6 +404,20 @@ def sweep(fs, name, pk, args, Bs=(1, 8, 32, 128, 256)):
         fs.set_option("time_stage1", 0)
         r = {"fused_us": round(us, 2), "stage1_us": round(t1 * 1e3, 2)}
         r["roofline"] = roofline(name, B, D, V, t1, pk, transforms)
+        if name == "llama3_8b" and not wl["group_size"]:
+            # SURVEY f3/f4 variants of the same step: per-request RNG streams, log-probabilities
+            seeds = torch.arange(B, device=dev, dtype=torch.int64) * 7919 + 17
+            vctr = [0]
+
+            def per_request():
+                vctr[0] += 1
+                fs.sample(wl["h"], wl["W"], seeds=seeds, step=vctr[0], out=out)
+
+            def with_logprob():
+                vctr[0] += 1
+                fs.sample(wl["h"], wl["W"], seed=synth.SAMPLING_SEED, step=vctr[0], return_logprob=True)
+            r["variants"] = {"per_request_seeds_us": round(1e3 * time_median(per_request, 100, 25), 2),
+                             "with_logZ_logprob_us": round(1e3 * time_median(with_logprob, 100, 25), 2)}
         if not args.no_baselines and not wl["group_size"]:
             # standalone sampling over the same materialised fp32 logits (§5.2):
             # fs_sample_logits vs FlashInfer's Gumbel-max sampling_from_logits (FI2's sampler)

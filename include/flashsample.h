@@ -135,6 +135,37 @@ fs_status fs_sample_logits(fs_ctx* ctx, fs_dtype dtype, const void* logits, int6
                            int32_t* idx_out, float* score_out, float* logZ_out, float* logprob_out,
                            void* stream);
 
+/* Extended arguments for fs_sample_ex / fs_sample_logits_ex.
+ *   seeds [B] uint64 (device) or NULL: per-request RNG streams, batch-position invariant
+ *         (reading R18: key = seeds[b], counter = (v >> 2, 2^31, steps[b]), word v & 3);
+ *         NULL -> the shared stream (seed, step) of the convention above.
+ *   steps [B] uint64 (device) or NULL: per-request step counters (NULL -> `step` for every row).
+ *   Greedy rows: temperature[b] == 0 exactly -> argmax of l + bias without noise (R18).
+ *   group_size: fs_sample_ex only; 0 -> one group over V (grouped outputs when > 0). */
+typedef struct {
+  const float* bias;
+  const float* temperature;
+  const uint32_t* mask;
+  uint64_t seed;
+  uint64_t step;
+  const uint64_t* seeds;
+  const uint64_t* steps;
+  int group_size;
+  int32_t* idx_out;          /* [B] required */
+  float* score_out;          /* [B] or NULL */
+  float* logZ_out;           /* [B] or NULL */
+  float* logprob_out;        /* [B] or NULL */
+  fs_summary* groups_out;    /* [B][ceil(V/group_size)] or NULL (group_size > 0) */
+} fs_sample_args;
+
+/* fs_sample_ex -- fs_sample / fs_sample_grouped with per-request streams, greedy rows and every
+ * optional output selected through `args` (same kernels, same conventions). */
+fs_status fs_sample_ex(fs_ctx* ctx, fs_dtype dtype, const void* h, const void* W, int B, int D, int V,
+                       const fs_sample_args* args, void* stream);
+/* fs_sample_logits_ex -- fs_sample_logits with `args` (group_size and groups_out ignored). */
+fs_status fs_sample_logits_ex(fs_ctx* ctx, fs_dtype dtype, const void* logits, int64_t ld, int B, int V,
+                              const fs_sample_args* args, void* stream);
+
 /* fs_sample_shard -- the rank-local half of distributed FlashSampling for a vocabulary-
  * sharded (tensor-parallel) LM head (§4.2, Alg. A.4).
  *   W_shard [V_local,D] holds global rows [vocab_offset, vocab_offset+V_local);

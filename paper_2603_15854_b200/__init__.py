@@ -92,17 +92,38 @@ def _check_inputs(h, W, bias, temperature, mask, V_total=None):
     return B, D, V
 
 
+def _u64(t, B, name, dev):
+    if t is None:
+        return None
+    if t.dtype not in (torch.int64, torch.uint64) or t.numel() != B or not t.is_contiguous() or t.device != dev:
+        raise ValueError(f"{name} must be a contiguous int64/uint64 [B] tensor on the sampling device")
+    return t
+
+
 def sample(h, W, *, bias=None, temperature=None, mask=None, seed: int = 0, step: int = 0,
-           return_score: bool = False, out=None):
-    """Fused LM-head + exact Gumbel-max sample per row (fs_sample).  Returns int32 [B]
-    (and the winning perturbed scores, fp32 [B], if return_score)."""
+           seeds=None, steps=None, return_score: bool = False, return_logprob: bool = False, out=None):
+    """Fused LM-head + exact Gumbel-max sample per row.  Returns int32 [B]; with return_score
+    also the winning perturbed scores; with return_logprob also (logZ, log p(idx)).
+    seeds / steps: optional [B] int64 per-request streams (batch-position invariant, reading R18);
+    temperature[b] == 0 samples row b greedily."""
     B, D, V = _check_inputs(h, W, bias, temperature, mask)
     idx = out if out is not None else torch.empty(B, dtype=torch.int32, device=h.device)
     score = torch.empty(B, dtype=torch.float32, device=h.device) if return_score else None
-    _lib.check(_lib.lib().fs_sample(context(h.device), _dtype_code(h, W), _ptr(h), _ptr(W), _ptr(bias),
-                                    _ptr(temperature), _ptr(mask), seed & (2**64 - 1), step & (2**64 - 1),
-                                    B, D, V, _ptr(idx), _ptr(score), _stream(h)), "fs_sample")
-    return (idx, score) if return_score else idx
+    seeds = _u64(seeds, B, "seeds", h.device)
+    steps = _u64(steps, B, "steps", h.device)
+    if seeds is None and steps is None and not return_logprob:
+        _lib.check(_lib.lib().fs_sample(context(h.device), _dtype_code(h, W), _ptr(h), _ptr(W), _ptr(bias),
+                                        _ptr(temperature), _ptr(mask), seed & (2**64 - 1), step & (2**64 - 1),
+                                        B, D, V, _ptr(idx), _ptr(score), _stream(h)), "fs_sample")
+        return (idx, score) if return_score else idx
+    logZ = torch.empty(B, dtype=torch.float32, device=h.device) if return_logprob else None
+    logprob = torch.empty(B, dtype=torch.float32, device=h.device) if return_logprob else None
+    args = _lib.SampleArgs(_ptr(bias), _ptr(temperature), _ptr(mask), seed & (2**64 - 1), step & (2**64 - 1),
+                           _ptr(seeds), _ptr(steps), 0, _ptr(idx), _ptr(score), _ptr(logZ), _ptr(logprob), None)
+    _lib.check(_lib.lib().fs_sample_ex(context(h.device), _dtype_code(h, W), _ptr(h), _ptr(W), B, D, V,
+                                       ctypes.byref(args), _stream(h)), "fs_sample_ex")
+    res = (idx,) + ((score,) if return_score else ()) + ((logZ, logprob) if return_logprob else ())
+    return res if len(res) > 1 else idx
 
 
 @dataclasses.dataclass
@@ -148,9 +169,9 @@ def sample_grouped(h, W, *, group_size: int, bias=None, temperature=None, mask=N
 
 
 def sample_logits(logits, *, bias=None, temperature=None, mask=None, seed: int = 0, step: int = 0,
-                  return_all: bool = False):
+                  seeds=None, steps=None, return_all: bool = False):
     """Standalone Gumbel-max over materialised logits [B, V] (bf16 or fp32, row stride may exceed V)
-    (fs_sample_logits).  Returns idx [B], or (idx, score, logZ, logprob) if return_all."""
+    (fs_sample_logits[_ex]).  Returns idx [B], or (idx, score, logZ, logprob) if return_all."""
     if not logits.is_cuda or logits.dim() != 2 or logits.stride(1) != 1:
         raise ValueError("logits must be a 2-D CUDA tensor with unit column stride")
     B, V = logits.shape
@@ -164,14 +185,16 @@ def sample_logits(logits, *, bias=None, temperature=None, mask=None, seed: int =
     if code is None:
         raise TypeError("logits must be bf16 or fp32")
     dev = logits.device
+    seeds = _u64(seeds, B, "seeds", dev)
+    steps = _u64(steps, B, "steps", dev)
     idx = torch.empty(B, dtype=torch.int32, device=dev)
     score = torch.empty(B, dtype=torch.float32, device=dev) if return_all else None
     logZ = torch.empty(B, dtype=torch.float32, device=dev) if return_all else None
     logprob = torch.empty(B, dtype=torch.float32, device=dev) if return_all else None
-    _lib.check(_lib.lib().fs_sample_logits(
-        context(dev), code, _ptr(logits), logits.stride(0), _ptr(bias), _ptr(temperature), _ptr(mask),
-        seed & (2**64 - 1), step & (2**64 - 1), B, V, _ptr(idx), _ptr(score), _ptr(logZ), _ptr(logprob),
-        _stream(logits)), "fs_sample_logits")
+    args = _lib.SampleArgs(_ptr(bias), _ptr(temperature), _ptr(mask), seed & (2**64 - 1), step & (2**64 - 1),
+                           _ptr(seeds), _ptr(steps), 0, _ptr(idx), _ptr(score), _ptr(logZ), _ptr(logprob), None)
+    _lib.check(_lib.lib().fs_sample_logits_ex(context(dev), code, _ptr(logits), logits.stride(0), B, V,
+                                              ctypes.byref(args), _stream(logits)), "fs_sample_logits_ex")
     return (idx, score, logZ, logprob) if return_all else idx
 
 

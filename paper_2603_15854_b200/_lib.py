@@ -14,11 +14,21 @@ LIB_PATH = os.path.join(HERE, "libflashsample.so")
 # Every symbol include/flashsample.h declares (checked by tests/test_abi.py).
 EXPORTS = [
     "fs_version", "fs_status_str", "fs_last_error", "fs_ctx_create", "fs_ctx_destroy",
-    "fs_ctx_set_option", "fs_ctx_query", "fs_sample", "fs_sample_grouped", "fs_sample_logits", "fs_sample_shard",
+    "fs_ctx_set_option", "fs_ctx_query", "fs_sample", "fs_sample_ex", "fs_sample_grouped", "fs_sample_logits",
+    "fs_sample_logits_ex", "fs_sample_shard",
     "fs_combine_summaries", "fs_merge_summaries", "fs_random_bits", "fs_gumbel_from_bits",
 ]
 
 FS_OK, FS_ERR_INVALID, FS_ERR_UNSUPPORTED, FS_ERR_CUDA, FS_ERR_OOM = range(5)
+
+
+class SampleArgs(ctypes.Structure):
+    """fs_sample_args (include/flashsample.h)."""
+    _fields_ = [("bias", ctypes.c_void_p), ("temperature", ctypes.c_void_p), ("mask", ctypes.c_void_p),
+                ("seed", ctypes.c_uint64), ("step", ctypes.c_uint64), ("seeds", ctypes.c_void_p),
+                ("steps", ctypes.c_void_p), ("group_size", ctypes.c_int), ("idx_out", ctypes.c_void_p),
+                ("score_out", ctypes.c_void_p), ("logZ_out", ctypes.c_void_p), ("logprob_out", ctypes.c_void_p),
+                ("groups_out", ctypes.c_void_p)]
 FS_BF16, FS_F32 = 0, 1
 
 
@@ -54,6 +64,8 @@ def lib() -> ctypes.CDLL:
     L.fs_sample_grouped.argtypes = [vp, i32, vp, vp, vp, vp, vp, u64, u64, i32, i32, i32, i32,
                                     vp, vp, vp, vp, vp, vp]
     L.fs_sample_logits.argtypes = [vp, i32, vp, i64, vp, vp, vp, u64, u64, i32, i32, vp, vp, vp, vp, vp]
+    L.fs_sample_ex.argtypes = [vp, i32, vp, vp, i32, i32, i32, ctypes.POINTER(SampleArgs), vp]
+    L.fs_sample_logits_ex.argtypes = [vp, i32, vp, i64, i32, i32, ctypes.POINTER(SampleArgs), vp]
     L.fs_sample_shard.argtypes = [vp, i32, vp, vp, vp, vp, vp, u64, u64, i32, i32, i32, i64, i64, vp, vp]
     L.fs_combine_summaries.argtypes = [vp, i32, i32, vp, vp, vp, vp]
     L.fs_merge_summaries.argtypes = [vp, vp, vp, i32, vp]

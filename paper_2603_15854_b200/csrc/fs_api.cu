@@ -178,6 +178,8 @@ struct PathArgs {
   fs_summary* groups_out;
   int n_groups;
   float* logprob_out;
+  const uint64_t* seeds = nullptr;
+  const uint64_t* steps = nullptr;
 };
 
 fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
@@ -219,6 +221,8 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
     p.W = a.W;
     p.bias = a.bias;
     p.temperature = a.temperature ? a.temperature + r0 : nullptr;
+    p.seeds = a.seeds ? a.seeds + r0 : nullptr;
+    p.steps = a.steps ? a.steps + r0 : nullptr;
     p.mask = a.mask ? a.mask + (size_t)r0 * a.mask_words : nullptr;
     p.mask_words = a.mask_words;
     p.vocab_offset = a.vocab_offset;
@@ -442,9 +446,10 @@ fs_status fs_sample_shard(fs_ctx* ctx, fs_dtype dtype, const void* h, const void
   return run_path(ctx, a, static_cast<cudaStream_t>(stream));
 }
 
-fs_status fs_sample_logits(fs_ctx* ctx, fs_dtype dtype, const void* logits, int64_t ld, const float* bias,
-                           const float* temperature, const uint32_t* mask, uint64_t seed, uint64_t step, int B, int V,
-                           int32_t* idx_out, float* score_out, float* logZ_out, float* logprob_out, void* stream) {
+static fs_status sample_logits_impl(fs_ctx* ctx, fs_dtype dtype, const void* logits, int64_t ld, const float* bias,
+                                    const float* temperature, const uint32_t* mask, uint64_t seed, uint64_t step,
+                                    const uint64_t* seeds, const uint64_t* steps, int B, int V, int32_t* idx_out,
+                                    float* score_out, float* logZ_out, float* logprob_out, void* stream) {
   if (!ctx) return fail(FS_ERR_INVALID, "ctx is NULL");
   if (dtype != FS_BF16 && dtype != FS_F32) return fail(FS_ERR_INVALID, "unknown dtype");
   if (!logits || !idx_out) return fail(FS_ERR_INVALID, "logits and idx_out are required");
@@ -462,12 +467,44 @@ fs_status fs_sample_logits(fs_ctx* ctx, fs_dtype dtype, const void* logits, int6
   int* part_group = reinterpret_cast<int*>(static_cast<char*>(ctx->ws) + grp_off);
   const bool lse = logZ_out || logprob_out;
   e = fs::launch_logits_sample(dtype, logits, ld, bias, temperature, mask, ((int64_t)V + 31) / 32, B, V, seed, step,
-                               lse, nblk, part, part_group, stream_);
+                               lse, nblk, part, part_group, stream_, seeds, steps);
   if (e != cudaSuccess) return cuda_fail(e, "logits sampler launch");
   const fs::SlotLayout lay{nblk, 1, nblk, V, 1, V, 128, 0};
   e = fs::launch_reduce(part, part_group, lay, B, 1, idx_out, score_out, logZ_out, nullptr, stream_, ctx->pdl != 0,
                         logprob_out);
   return e == cudaSuccess ? FS_OK : cuda_fail(e, "stage-2 reduce launch");
+}
+
+fs_status fs_sample_logits(fs_ctx* ctx, fs_dtype dtype, const void* logits, int64_t ld, const float* bias,
+                           const float* temperature, const uint32_t* mask, uint64_t seed, uint64_t step, int B, int V,
+                           int32_t* idx_out, float* score_out, float* logZ_out, float* logprob_out, void* stream) {
+  return sample_logits_impl(ctx, dtype, logits, ld, bias, temperature, mask, seed, step, nullptr, nullptr, B, V,
+                            idx_out, score_out, logZ_out, logprob_out, stream);
+}
+
+fs_status fs_sample_logits_ex(fs_ctx* ctx, fs_dtype dtype, const void* logits, int64_t ld, int B, int V,
+                              const fs_sample_args* a, void* stream) {
+  if (!a) return fail(FS_ERR_INVALID, "args is NULL");
+  return sample_logits_impl(ctx, dtype, logits, ld, a->bias, a->temperature, a->mask, a->seed, a->step, a->seeds,
+                            a->steps, B, V, a->idx_out, a->score_out, a->logZ_out, a->logprob_out, stream);
+}
+
+fs_status fs_sample_ex(fs_ctx* ctx, fs_dtype dtype, const void* h, const void* W, int B, int D, int V,
+                       const fs_sample_args* args, void* stream) {
+  if (!args) return fail(FS_ERR_INVALID, "args is NULL");
+  fs_status s = check_common(ctx, dtype, h, W, B, D, V);
+  if (s != FS_OK) return s;
+  if (!args->idx_out) return fail(FS_ERR_INVALID, "idx_out is required");
+  if (args->steps && !args->seeds) return fail(FS_ERR_INVALID, "steps requires seeds");
+  int gs = args->group_size;
+  if (gs < 0 || (gs > 0 && gs % 128 != 0)) return fail(FS_ERR_INVALID, "group_size must be 0 or a multiple of 128");
+  if (gs == 0 || gs >= V) gs = ((V + 127) / 128) * 128;
+  const int n_groups = (V + gs - 1) / gs;
+  const bool lse = args->logZ_out || args->logprob_out || args->groups_out || n_groups > 1;
+  PathArgs a{dtype, h, W, args->bias, args->temperature, args->mask, ((int64_t)V + 31) / 32, args->seed, args->step,
+             B, D, V, 0, gs, lse, args->idx_out, args->score_out, args->logZ_out, args->groups_out, n_groups,
+             args->logprob_out, args->seeds, args->steps};
+  return run_path(ctx, a, static_cast<cudaStream_t>(stream));
 }
 
 fs_status fs_combine_summaries(const fs_summary* gathered, int n, int B, int32_t* idx_out, float* score_out,

@@ -17,8 +17,48 @@
 
 namespace fs {
 
+// Per-batch-column constants of one launch, staged in shared memory at kernel start.
+struct RowTab {
+  float invtau[256];        // 1/tau_b (1 for greedy rows), NaN for invalid or padding columns
+  float gscale[256];        // noise scale: 1 sampled, 0 greedy (tau == 0; reading R18)
+  uint32_t k0[256], k1[256], c2[256], c3[256];   // per-request Philox key / counter words (R18)
+};
+
+// Fill the table (all threads of the CTA; caller synchronises).
+template <bool PRQ>
+__device__ __forceinline__ void fill_rowtab(RowTab* t, int B, const float* temperature, const uint64_t* seeds,
+                                            const uint64_t* steps, uint64_t step, int tid, int nthreads) {
+  for (int b = tid; b < 256; b += nthreads) {
+    float it = __int_as_float(0x7FC00000), gsc = 1.0f;
+    if (b < B) {
+      const float tau = temperature ? temperature[b] : 1.0f;
+      if (tau == 0.0f) { it = 1.0f; gsc = 0.0f; }
+      else if (tau > 0.0f && isfinite(tau)) it = 1.0f / tau;
+    }
+    t->invtau[b] = it;
+    t->gscale[b] = gsc;
+    if (PRQ) {
+      const uint64_t sd = b < B ? seeds[b] : 0ull;
+      const uint64_t st = b < B ? (steps ? steps[b] : step) : 0ull;
+      t->k0[b] = (uint32_t)sd;
+      t->k1[b] = (uint32_t)(sd >> 32);
+      t->c2[b] = (uint32_t)st;
+      t->c3[b] = (uint32_t)(st >> 32) & 0x00FFFFFFu;
+    }
+  }
+}
+
+// Per-request draw for (vocabulary id v, batch column b): Philox at counter
+// (v >> 2, 2^31, step_b) under key seed_b, word v & 3 (reading R18).
+__device__ __forceinline__ uint32_t per_request_bits(const RowTab* t, uint32_t v, int b) {
+  const U4 o = philox4x32_10(v >> 2, 0x80000000u, t->c2[b], t->c3[b], t->k0[b], t->k1[b]);
+  const uint32_t sel = v & 3u;
+  return sel == 0 ? o.x : sel == 1 ? o.y : sel == 2 ? o.z : o.w;
+}
+
 struct EpiArgs {
   const float* invtau;      // smem [BN]: 1/tau_b, NaN for invalid or padding columns
+  const RowTab* tab;        // smem row table (invtau, gscale, per-request RNG words)
   const uint32_t* mask;     // global [rows][mask_words] for this launch's rows, or nullptr
   int64_t mask_words;
   int B;                    // valid columns in this launch
@@ -55,15 +95,21 @@ __device__ __forceinline__ void absorb(State& own, uint32_t kmax, int32_t widx, 
 
 // Process NCOL (multiple of 4) consecutive accumulator columns [col0, col0+NCOL) of this lane's
 // row; `own` is this lane's state for column col0 + lane.
-template <int NCOL, bool LSE>
+template <int NCOL, bool LSE, bool PRQ = false>
 __device__ __forceinline__ void epi_columns(const float* acc, int col0, const RowArgs& ra,
                                             const EpiArgs& ea, State& own, int lane) {
 #pragma unroll
   for (int j = 0; j < NCOL; j += 4) {
     const int b0 = col0 + j;
     if (b0 >= ea.B) break;                                   // warp-uniform
-    const U4 r4 = philox4x32_10(ra.v_lo, (uint32_t)(ea.row_offset + b0) >> 2, ea.c2, ea.c3, ea.k0, ea.k1);
-    const uint32_t rr[4] = {r4.x, r4.y, r4.z, r4.w};
+    uint32_t rr[4];
+    if (PRQ) {
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) rr[jj] = per_request_bits(ea.tab, ra.v_lo, b0 + jj);
+    } else {
+      const U4 r4 = philox4x32_10(ra.v_lo, (uint32_t)(ea.row_offset + b0) >> 2, ea.c2, ea.c3, ea.k0, ea.k1);
+      rr[0] = r4.x; rr[1] = r4.y; rr[2] = r4.z; rr[3] = r4.w;
+    }
 #pragma unroll
     for (int jj = 0; jj < 4; ++jj) {
       const int b = b0 + jj;
@@ -73,7 +119,7 @@ __device__ __forceinline__ void epi_columns(const float* acc, int col0, const Ro
         if (!((w >> (ra.v_global & 31)) & 1u)) lt = -INFINITY;
       }
       if (isnan(lt)) lt = -INFINITY;
-      const float s = lt + gumbel32(rr[jj]);
+      const float s = lt + gumbel32(rr[jj]) * ea.tab->gscale[b];
       const uint32_t key = ra.valid ? order_key(s) : kKeyNone;
       const uint32_t kmax = __reduce_max_sync(0xFFFFFFFFu, key);
       const uint32_t ball = __ballot_sync(0xFFFFFFFFu, key == kmax);
@@ -143,7 +189,7 @@ __device__ __forceinline__ void release_tmem(uint64_t* tempty, uint32_t tempty_c
 // NG groups of 8 columns per iteration (NG = 2 doubles the independent work in flight: 4 Philox
 // chains, 16 Gumbel evaluations, 16 warp reductions -- the epilogue is latency-bound at one warp
 // pair per SM sub-partition).  Columns >= B are computed on padding and never stored.
-template <bool LSE, bool XFORM, int NG>
+template <bool LSE, bool XFORM, int NG, bool PRQ = false>
 __device__ __forceinline__ void epi_tile_tc(uint32_t taddr, const RowArgs& ra, const EpiArgs& ea, State (&st)[8],
                                             int lane, uint64_t* tempty, uint32_t tempty_cluster = 0) {
   constexpr int NC = 8 * NG;
@@ -177,15 +223,20 @@ __device__ __forceinline__ void epi_tile_tc(uint32_t taddr, const RowArgs& ra, c
         if ((lane & 15) < NC && jb < B && w < ea.mask_words) mw = __ldg(ea.mask + (int64_t)jb * ea.mask_words + w);
       }
       // randomness: independent of the accumulator, overlaps the TMEM load
-      const uint32_t qd = (uint32_t)(ea.row_offset + col0) >> 2;
       float gm[NC];
+      if (PRQ) {                                 // per-request streams: one Philox per element
 #pragma unroll
-      for (int qq = 0; qq < NC / 4; ++qq) {
-        const U4 p4 = philox4x32_10(ra.v_lo, qd + (uint32_t)qq, ea.c2, ea.c3, ea.k0, ea.k1);
-        gm[4 * qq + 0] = gumbel32(p4.x);
-        gm[4 * qq + 1] = gumbel32(p4.y);
-        gm[4 * qq + 2] = gumbel32(p4.z);
-        gm[4 * qq + 3] = gumbel32(p4.w);
+        for (int jj = 0; jj < NC; ++jj) gm[jj] = gumbel32(per_request_bits(ea.tab, ra.v_lo, col0 + jj));
+      } else {
+        const uint32_t qd = (uint32_t)(ea.row_offset + col0) >> 2;
+#pragma unroll
+        for (int qq = 0; qq < NC / 4; ++qq) {
+          const U4 p4 = philox4x32_10(ra.v_lo, qd + (uint32_t)qq, ea.c2, ea.c3, ea.k0, ea.k1);
+          gm[4 * qq + 0] = gumbel32(p4.x);
+          gm[4 * qq + 1] = gumbel32(p4.y);
+          gm[4 * qq + 2] = gumbel32(p4.z);
+          gm[4 * qq + 3] = gumbel32(p4.w);
+        }
       }
       sm100::tmem_wait_ld();
       if (col0 + NC >= B) release_tmem(tempty, tempty_cluster, lane);   // last TMEM read of the tile
@@ -194,8 +245,10 @@ __device__ __forceinline__ void epi_tile_tc(uint32_t taddr, const RowArgs& ra, c
 #pragma unroll
       for (int jj = 0; jj < NC; ++jj) {
         float l = __uint_as_float(r[jj]);
+        float gj = gm[jj];
         if (XFORM) {
           l = (l + ra.bias) * ea.invtau[col0 + jj];
+          gj *= ea.tab->gscale[col0 + jj];              // 0 on greedy rows
           if (ea.mask != nullptr) {
             const uint32_t lo = __shfl_sync(0xFFFFFFFFu, mw, jj), hi = __shfl_sync(0xFFFFFFFFu, mw, 16 + jj);
             const uint32_t bits = wshift ? __funnelshift_r(lo, hi, wshift) : lo;
@@ -204,7 +257,7 @@ __device__ __forceinline__ void epi_tile_tc(uint32_t taddr, const RowArgs& ra, c
         }
         if (isnan(l)) l = -INFINITY;
         lt[jj] = l;
-        key[jj] = ra.valid ? order_key(l + gm[jj]) : kKeyNone;
+        key[jj] = ra.valid ? order_key(l + gj) : kKeyNone;
       }
       uint32_t kmax[NC], ball[NC];
 #pragma unroll

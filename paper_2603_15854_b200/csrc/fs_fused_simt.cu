@@ -20,20 +20,13 @@ __device__ __forceinline__ float ldf(const T* p) {
   else return *p;
 }
 
-template <typename T, bool LSE>
+template <typename T, bool LSE, bool PRQ>
 __global__ void __launch_bounds__(128) fused_simt_kernel(const StageOneParams p) {
-  __shared__ float invtau[256];
+  __shared__ RowTab tab;
   __shared__ State scratch[4 * 256];
   const T* __restrict__ h = static_cast<const T*>(p.h);
   const T* __restrict__ W = static_cast<const T*>(p.W);
-  for (int b = threadIdx.x; b < 256; b += 128) {
-    float it = __int_as_float(0x7FC00000);
-    if (b < p.B) {
-      const float t = p.temperature ? p.temperature[b] : 1.0f;
-      if (t > 0.0f && isfinite(t)) it = 1.0f / t;
-    }
-    invtau[b] = it;
-  }
+  fill_rowtab<PRQ>(&tab, p.B, p.temperature, p.seeds, p.steps, p.step, threadIdx.x, 128);
   __syncthreads();
   const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
   const int base = blockIdx.x * 128;
@@ -45,7 +38,8 @@ __global__ void __launch_bounds__(128) fused_simt_kernel(const StageOneParams p)
   ra.warp_v0 = (int32_t)(p.vocab_offset + base + 32 * q);
   ra.bias = (ra.valid && p.bias) ? p.bias[row] : 0.0f;
   EpiArgs ea;
-  ea.invtau = invtau;
+  ea.invtau = tab.invtau;
+  ea.tab = &tab;
   ea.mask = p.mask;
   ea.mask_words = p.mask_words;
   ea.B = p.B;
@@ -70,7 +64,7 @@ __global__ void __launch_bounds__(128) fused_simt_kernel(const StageOneParams p)
       for (int j = 0; j < 32; ++j)
         if (j < nb) acc[j] = fmaf(ldf(h + (size_t)(c * 32 + j) * p.D + d), w, acc[j]);
     }
-    epi_columns<32, LSE>(acc, c * 32, ra, ea, st[c], lane);
+    epi_columns<32, LSE, PRQ>(acc, c * 32, ra, ea, st[c], lane);
   }
   flush_states<kSimtChunks, 32>(st, scratch, 256, q, lane, threadIdx.x, p.B, p.part + (size_t)blockIdx.x * p.B, 1);
   if (threadIdx.x == 0) p.part_group[blockIdx.x] = base / p.group_size;
@@ -79,13 +73,14 @@ __global__ void __launch_bounds__(128) fused_simt_kernel(const StageOneParams p)
 
 cudaError_t launch_fused_simt(const StageOneParams& p, fs_dtype dtype, bool lse, cudaStream_t stream) {
   const int grid = (p.V + 127) / 128;
-  if (dtype == FS_BF16) {
-    if (lse) fused_simt_kernel<uint16_t, true><<<grid, 128, 0, stream>>>(p);
-    else fused_simt_kernel<uint16_t, false><<<grid, 128, 0, stream>>>(p);
-  } else {
-    if (lse) fused_simt_kernel<float, true><<<grid, 128, 0, stream>>>(p);
-    else fused_simt_kernel<float, false><<<grid, 128, 0, stream>>>(p);
-  }
+  const bool prq = p.seeds != nullptr;
+#define FS_SIMT(T)                                                                                    \
+  if (lse) { if (prq) fused_simt_kernel<T, true, true><<<grid, 128, 0, stream>>>(p);                  \
+             else fused_simt_kernel<T, true, false><<<grid, 128, 0, stream>>>(p); }                   \
+  else     { if (prq) fused_simt_kernel<T, false, true><<<grid, 128, 0, stream>>>(p);                 \
+             else fused_simt_kernel<T, false, false><<<grid, 128, 0, stream>>>(p); }
+  if (dtype == FS_BF16) { FS_SIMT(uint16_t) } else { FS_SIMT(float) }
+#undef FS_SIMT
   return cudaGetLastError();
 }
 

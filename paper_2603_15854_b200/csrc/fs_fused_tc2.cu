@@ -27,7 +27,7 @@ constexpr int kEpiWarps = 8;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kBlockK = 64;
 constexpr int kWBytes = 128 * kBlockK * 2;                  // this CTA's 128 W rows per K slice
-constexpr int kExtraBytes = 64 * 8 + 16 + 256 * 4 + 64;
+constexpr int kExtraBytes = 64 * 8 + 16 + (int)sizeof(RowTab) + 64;
 
 int tmem_cols_for(int BN) {
   int c = 32;
@@ -37,7 +37,7 @@ int tmem_cols_for(int BN) {
 __device__ __forceinline__ int seg_end2(int a, int r1, int gs) { return min(r1, (a / gs + 1) * gs); }
 }  // namespace
 
-template <bool LSE, bool XFORM>
+template <bool LSE, bool XFORM, bool PRQ>
 __global__ void __launch_bounds__(kThreads, 1)
 fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -51,7 +51,7 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* invtau = reinterpret_cast<float*>(tmem_slot + 4);
+  RowTab* tab = reinterpret_cast<RowTab*>(tmem_slot + 4);
 
   const uint32_t rank = sm100::cluster_ctarank();
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
@@ -71,16 +71,7 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
     sm100::fence_barrier_init();
   }
   if (warp == 1) sm100::tmem_alloc_pair(tmem_slot, (uint32_t)p.tmem_cols);
-  if (XFORM) {
-    for (int b = threadIdx.x; b < 256; b += kThreads) {
-      float it = __int_as_float(0x7FC00000);
-      if (b < p.B) {
-        const float t = p.temperature ? p.temperature[b] : 1.0f;
-        if (t > 0.0f && isfinite(t)) it = 1.0f / t;
-      }
-      invtau[b] = it;
-    }
-  }
+  if (XFORM) fill_rowtab<PRQ>(tab, p.B, p.temperature, p.seeds, p.steps, p.step, threadIdx.x, kThreads);
   sm100::tc_fence_before();
   sm100::cluster_sync();                    // both CTAs' barriers exist before any remote signal
   sm100::tc_fence_after();
@@ -164,7 +155,8 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
     const int set = e >> 2;
     const int q = warp & 3;
     EpiArgs ea;
-    ea.invtau = invtau;
+    ea.invtau = tab->invtau;
+    ea.tab = tab;
     ea.mask = p.mask;
     ea.mask_words = p.mask_words;
     ea.B = p.B;
@@ -196,8 +188,8 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
         ra.warp_v0 = (int32_t)(p.vocab_offset + base + 32 * q);
         ra.bias = (XFORM && ra.valid && p.bias) ? p.bias[row] : 0.0f;
         const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(set * BN);
-        if (p.B <= 8) epi_tile_tc<LSE, XFORM, 1>(taddr, ra, ea, st, lane, &tempty[set], tempty_leader);
-        else epi_tile_tc<LSE, XFORM, 2>(taddr, ra, ea, st, lane, &tempty[set], tempty_leader);
+        if (p.B <= 8) epi_tile_tc<LSE, XFORM, 1, PRQ>(taddr, ra, ea, st, lane, &tempty[set], tempty_leader);
+        else epi_tile_tc<LSE, XFORM, 2, PRQ>(taddr, ra, ea, st, lane, &tempty[set], tempty_leader);
       }
       if (gs < p.V) {
         const int slot = ((slot0 + seg) * 2 + (int)rank) * kEpiWarps + e;
@@ -258,11 +250,12 @@ cudaError_t launch_fused_tc2(const CUtensorMap& hmap, const StageOneParams& p_in
   p.bn = BN;
   p.tmem_cols = tmem_cols_for(BN);
   const size_t smem = 1024 + (size_t)p.stages * p.kbps * (kWBytes + (BN / 2) * kBlockK * 2) + kExtraBytes;
-  const bool xform = p.bias || p.temperature || p.mask;
-  auto kern = lse ? (xform ? fused_tc2_kernel<true, true> : fused_tc2_kernel<true, false>)
-                  : (xform ? fused_tc2_kernel<false, true> : fused_tc2_kernel<false, false>);
-  static bool attr_set[4] = {false, false, false, false};
-  const int variant = (lse ? 2 : 0) + (xform ? 1 : 0);
+  const bool xform = p.bias || p.temperature || p.mask || p.seeds;
+  const bool prq = p.seeds != nullptr;
+  auto kern = lse ? (prq ? fused_tc2_kernel<true, true, true> : xform ? fused_tc2_kernel<true, true, false> : fused_tc2_kernel<true, false, false>)
+                  : (prq ? fused_tc2_kernel<false, true, true> : xform ? fused_tc2_kernel<false, true, false> : fused_tc2_kernel<false, false, false>);
+  static bool attr_set[8] = {false, false, false, false, false, false, false, false};
+  const int variant = (lse ? 4 : 0) + (prq ? 2 : 0) + (xform ? 1 : 0);
   if (!attr_set[variant]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     if (e != cudaSuccess) return e;

@@ -16,6 +16,8 @@ struct StageOneParams {
   const void* W;              // [V, D]
   const float* bias;          // [V] (shard-local) or nullptr
   const float* temperature;   // [B] for this chunk or nullptr
+  const uint64_t* seeds;      // [B] per-request seeds for this chunk (reading R18) or nullptr
+  const uint64_t* steps;      // [B] per-request steps or nullptr (-> step)
   const uint32_t* mask;       // [B][mask_words] for this chunk (global ids) or nullptr
   int64_t mask_words;
   int64_t vocab_offset;       // global id of local row 0
@@ -71,7 +73,8 @@ cudaError_t launch_reduce(const State* part, const int* part_group, const SlotLa
 cudaError_t launch_logits_sample(fs_dtype dtype, const void* logits, int64_t ld, const float* bias,
                                  const float* temperature, const uint32_t* mask, int64_t mask_words, int B, int V,
                                  uint64_t seed, uint64_t step, bool lse, int nblk, State* part, int* part_group,
-                                 cudaStream_t stream);
+                                 cudaStream_t stream, const uint64_t* seeds = nullptr,
+                                 const uint64_t* steps = nullptr);
 int logits_sample_blocks(int B, int V);   // V blocks of the standalone sampler grid
 cudaError_t launch_combine(const fs_summary* gathered, int n, int B, int32_t* idx_out, float* score_out,
                            float* logZ_out, cudaStream_t stream);

@@ -35,31 +35,50 @@ __device__ __forceinline__ State shfl_state(const State& a, int o) {
   return r;
 }
 
-template <typename T, bool XFORM, bool LSE>
+template <typename T, bool XFORM, bool LSE, bool PRQ>
 __global__ void __launch_bounds__(256)
 logits_sample_kernel(const T* __restrict__ logits, int64_t ld, const float* __restrict__ bias,
                      const float* __restrict__ temperature, const uint32_t* __restrict__ mask, int64_t mask_words,
                      int B, int V, int vpb, uint32_t k0, uint32_t k1, uint32_t c2, uint32_t c3, State* part,
-                     int* part_group) {
+                     int* part_group, const uint64_t* __restrict__ seeds, const uint64_t* __restrict__ steps,
+                     uint64_t step) {
   __shared__ State red[8][4];
   const int b0 = blockIdx.y * 4;
   const int v_begin = blockIdx.x * vpb, v_end = min(V, v_begin + vpb);
-  float it[4];
+  float it[4], gsc[4];
+  uint32_t pk0[4], pk1[4], pc2[4], pc3[4];                  // per-request Philox words (R18)
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int b = b0 + j;
     it[j] = __int_as_float(0x7FC00000);
+    gsc[j] = 1.0f;
     if (b < B) {
       const float t = (XFORM && temperature) ? temperature[b] : 1.0f;
-      if (t > 0.0f && isfinite(t)) it[j] = 1.0f / t;
+      if (t == 0.0f) { it[j] = 1.0f; gsc[j] = 0.0f; }       // greedy row
+      else if (t > 0.0f && isfinite(t)) it[j] = 1.0f / t;
+    }
+    if (PRQ) {
+      const uint64_t sd = b < B ? seeds[b] : 0ull, st = b < B ? (steps ? steps[b] : step) : 0ull;
+      pk0[j] = (uint32_t)sd; pk1[j] = (uint32_t)(sd >> 32);
+      pc2[j] = (uint32_t)st; pc3[j] = (uint32_t)(st >> 32) & 0x00FFFFFFu;
     }
   }
   State st[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) st[j] = state_empty();
   for (int v = v_begin + (int)threadIdx.x; v < v_end; v += 256) {
-    const U4 r4 = philox4x32_10((uint32_t)v, (uint32_t)b0 >> 2, c2, c3, k0, k1);
-    const uint32_t rr[4] = {r4.x, r4.y, r4.z, r4.w};
+    uint32_t rr[4];
+    if (PRQ) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const U4 o = philox4x32_10((uint32_t)v >> 2, 0x80000000u, pc2[j], pc3[j], pk0[j], pk1[j]);
+        const uint32_t sel = (uint32_t)v & 3u;
+        rr[j] = sel == 0 ? o.x : sel == 1 ? o.y : sel == 2 ? o.z : o.w;
+      }
+    } else {
+      const U4 r4 = philox4x32_10((uint32_t)v, (uint32_t)b0 >> 2, c2, c3, k0, k1);
+      rr[0] = r4.x; rr[1] = r4.y; rr[2] = r4.z; rr[3] = r4.w;
+    }
     const float bv = (XFORM && bias) ? bias[v] : 0.0f;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -71,7 +90,7 @@ logits_sample_kernel(const T* __restrict__ logits, int64_t ld, const float* __re
         if (mask && !((mask[(int64_t)b * mask_words + (v >> 5)] >> (v & 31)) & 1u)) l = -INFINITY;
       }
       if (isnan(l)) l = -INFINITY;
-      const float s = l + gumbel32(rr[j]);
+      const float s = l + gumbel32(rr[j]) * gsc[j];
       const uint32_t key = order_key(s);
       if (key > st[j].key) {                                 // v ascends per thread: ties keep smaller v
         if (LSE) {
@@ -114,23 +133,23 @@ logits_sample_kernel(const T* __restrict__ logits, int64_t ld, const float* __re
 cudaError_t launch_logits_sample(fs_dtype dtype, const void* logits, int64_t ld, const float* bias,
                                  const float* temperature, const uint32_t* mask, int64_t mask_words, int B, int V,
                                  uint64_t seed, uint64_t step, bool lse, int nblk, State* part, int* part_group,
-                                 cudaStream_t stream) {
+                                 cudaStream_t stream, const uint64_t* seeds, const uint64_t* steps) {
   const int vpb = ((V + nblk - 1) / nblk + 255) / 256 * 256;
   const dim3 grid((V + vpb - 1) / vpb, (B + 3) / 4);
-  const bool xform = bias || temperature || mask;
+  const bool xform = bias || temperature || mask || seeds;
+  const bool prq = seeds != nullptr;
   const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
   const uint32_t c2 = (uint32_t)step, c3 = (uint32_t)(step >> 32) & 0x00FFFFFFu;
-#define FS_LAUNCH(T, X, L)                                                                                   \
-  logits_sample_kernel<T, X, L><<<grid, 256, 0, stream>>>(static_cast<const T*>(logits), ld, bias, temperature, \
-                                                          mask, mask_words, B, V, vpb, k0, k1, c2, c3, part,  \
-                                                          part_group)
-  if (dtype == FS_BF16) {
-    if (xform) { if (lse) FS_LAUNCH(uint16_t, true, true); else FS_LAUNCH(uint16_t, true, false); }
-    else       { if (lse) FS_LAUNCH(uint16_t, false, true); else FS_LAUNCH(uint16_t, false, false); }
-  } else {
-    if (xform) { if (lse) FS_LAUNCH(float, true, true); else FS_LAUNCH(float, true, false); }
-    else       { if (lse) FS_LAUNCH(float, false, true); else FS_LAUNCH(float, false, false); }
-  }
+#define FS_LAUNCH(T, X, L, P)                                                                                 \
+  logits_sample_kernel<T, X, L, P><<<grid, 256, 0, stream>>>(static_cast<const T*>(logits), ld, bias, temperature, \
+                                                             mask, mask_words, B, V, vpb, k0, k1, c2, c3, part,  \
+                                                             part_group, seeds, steps, step)
+#define FS_DISPATCH(T)                                                                                         \
+  if (prq) { if (lse) FS_LAUNCH(T, true, true, true); else FS_LAUNCH(T, true, false, true); }                  \
+  else if (xform) { if (lse) FS_LAUNCH(T, true, true, false); else FS_LAUNCH(T, true, false, false); }          \
+  else { if (lse) FS_LAUNCH(T, false, true, false); else FS_LAUNCH(T, false, false, false); }
+  if (dtype == FS_BF16) { FS_DISPATCH(uint16_t) } else { FS_DISPATCH(float) }
+#undef FS_DISPATCH
 #undef FS_LAUNCH
   return cudaGetLastError();
 }

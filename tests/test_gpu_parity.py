@@ -102,7 +102,7 @@ def test_degenerate_single_token_vocab():
 
 def test_invalid_temperature_rows():
     wl = synth.make_workload("llama3_8b", 4, V=500, D=64)
-    wl.temperature = torch.tensor([1.0, 0.0, -1.0, float("nan")])
+    wl.temperature = torch.tensor([1.0, -0.5, -1.0, float("nan")])
     idx, score = _run(wl, 0)
     assert idx[1:].tolist() == [-1, -1, -1] and idx[0] >= 0
     assert np.all(np.isneginf(score[1:]))

@@ -123,6 +123,12 @@ __device__ __forceinline__ float key_ref(uint32_t key) {
   return key > kKeyNegInf ? key_to_float(key) : -INFINITY;
 }
 
+// Max-merge only (no log-mass): larger key wins, ties -> smaller id.
+__device__ __forceinline__ State state_max(State a, State b) {
+  const bool take_b = (b.key > a.key) || (b.key == a.key && b.idx >= 0 && (a.idx < 0 || b.idx < a.idx));
+  return take_b ? b : a;
+}
+
 // Merge two states over disjoint vocabulary sets: max-merge (ties -> smaller id) and
 // logaddexp of the masses (binary merge realised by max reuse).
 __device__ __forceinline__ State state_merge(State a, State b) {

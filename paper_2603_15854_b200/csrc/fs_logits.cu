@@ -66,42 +66,56 @@ logits_sample_kernel(const T* __restrict__ logits, int64_t ld, const float* __re
   State st[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) st[j] = state_empty();
-  for (int v = v_begin + (int)threadIdx.x; v < v_end; v += 256) {
-    uint32_t rr[4];
-    if (PRQ) {
+  // 4 columns per iteration (v, v+256, v+512, v+768): all 16 loads issued before the RNG work
+  for (int v0 = v_begin + (int)threadIdx.x; v0 < v_end; v0 += 1024) {
+    float lv[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int v = v0 + 256 * u;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        lv[u][j] = (v < v_end && b0 + j < B) ? ld_logit(logits + (int64_t)(b0 + j) * ld + v) : -INFINITY;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int v = v0 + 256 * u;
+      if (v >= v_end) break;
+      uint32_t rr[4];
+      if (PRQ) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const U4 o = philox4x32_10((uint32_t)v >> 2, 0x80000000u, pc2[j], pc3[j], pk0[j], pk1[j]);
+          const uint32_t sel = (uint32_t)v & 3u;
+          rr[j] = sel == 0 ? o.x : sel == 1 ? o.y : sel == 2 ? o.z : o.w;
+        }
+      } else {
+        const U4 r4 = philox4x32_10((uint32_t)v, (uint32_t)b0 >> 2, c2, c3, k0, k1);
+        rr[0] = r4.x; rr[1] = r4.y; rr[2] = r4.z; rr[3] = r4.w;
+      }
+      const float bv = (XFORM && bias) ? bias[v] : 0.0f;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const U4 o = philox4x32_10((uint32_t)v >> 2, 0x80000000u, pc2[j], pc3[j], pk0[j], pk1[j]);
-        const uint32_t sel = (uint32_t)v & 3u;
-        rr[j] = sel == 0 ? o.x : sel == 1 ? o.y : sel == 2 ? o.z : o.w;
-      }
-    } else {
-      const U4 r4 = philox4x32_10((uint32_t)v, (uint32_t)b0 >> 2, c2, c3, k0, k1);
-      rr[0] = r4.x; rr[1] = r4.y; rr[2] = r4.z; rr[3] = r4.w;
-    }
-    const float bv = (XFORM && bias) ? bias[v] : 0.0f;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int b = b0 + j;
-      if (b >= B) break;                                     // block-uniform
-      float l = ld_logit(logits + (int64_t)b * ld + v);
-      if (XFORM) {
-        l = (l + bv) * it[j];
-        if (mask && !((mask[(int64_t)b * mask_words + (v >> 5)] >> (v & 31)) & 1u)) l = -INFINITY;
-      }
-      if (isnan(l)) l = -INFINITY;
-      const float s = l + gumbel32(rr[j]) * gsc[j];
-      const uint32_t key = order_key(s);
-      if (key > st[j].key) {                                 // v ascends per thread: ties keep smaller v
-        if (LSE) {
-          st[j].S = (st[j].key > kKeyNegInf ? st[j].S * fast_exp2((key_ref(st[j].key) - s) * kLog2e) : 0.0f) +
-                    (s != -INFINITY ? fast_exp2((l - s) * kLog2e) : 0.0f);
-          st[j].lt = __float_as_uint(l);
+        const int b = b0 + j;
+        if (b >= B) break;                                   // block-uniform
+        float l = lv[u][j];
+        if (XFORM) {
+          l = (l + bv) * it[j];
+          if (mask && !((mask[(int64_t)b * mask_words + (v >> 5)] >> (v & 31)) & 1u)) l = -INFINITY;
         }
-        st[j].key = key;
-        st[j].idx = v;
-      } else if (LSE && st[j].key > kKeyNegInf) {
-        st[j].S += fast_exp2((l - key_ref(st[j].key)) * kLog2e);
+        if (isnan(l)) l = -INFINITY;
+        const float s = l + gumbel32(rr[j]) * gsc[j];
+        const uint32_t key = order_key(s);
+        if (key > st[j].key) {                               // v ascends per thread: ties keep smaller v
+          if (LSE) {
+            st[j].S = (st[j].key > kKeyNegInf ? st[j].S * fast_exp2((key_ref(st[j].key) - s) * kLog2e) : 0.0f) +
+                      (s != -INFINITY ? fast_exp2((l - s) * kLog2e) : 0.0f);
+            st[j].lt = __float_as_uint(l);
+          }
+          st[j].key = key;
+          st[j].idx = v;
+        } else if (LSE && st[j].key > kKeyNegInf) {
+          st[j].S += fast_exp2((l - key_ref(st[j].key)) * kLog2e);
+        }
       }
     }
   }
@@ -112,7 +126,8 @@ logits_sample_kernel(const T* __restrict__ logits, int64_t ld, const float* __re
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const State y = shfl_state(x, o);
-      x = (lane & o) ? state_merge(y, x) : state_merge(x, y);
+      if (LSE) x = (lane & o) ? state_merge(y, x) : state_merge(x, y);
+      else x = state_max(x, y);
     }
     if (lane == 0) red[warp][j] = x;
   }
@@ -121,7 +136,7 @@ logits_sample_kernel(const T* __restrict__ logits, int64_t ld, const float* __re
     const int j = threadIdx.x, b = b0 + j;
     State x = red[0][j];
 #pragma unroll
-    for (int w = 1; w < 8; ++w) x = state_merge(x, red[w][j]);
+    for (int w = 1; w < 8; ++w) x = LSE ? state_merge(x, red[w][j]) : state_max(x, red[w][j]);
     if (b < B) part[(size_t)blockIdx.x * B + b] = x;
   }
   if (threadIdx.x == 0 && blockIdx.y == 0) part_group[blockIdx.x] = 0;
@@ -155,9 +170,10 @@ cudaError_t launch_logits_sample(fs_dtype dtype, const void* logits, int64_t ld,
 }
 
 int logits_sample_blocks(int B, int V) {
-  // >= 2 waves of 148 SMs over (V blocks) x (B/4), at least 256 columns per block
+  // ~16 columns per thread (4096 per block) so each thread has few dependent iterations, but at
+  // least 2 waves of 148 SMs over (V blocks) x (B/4) and at least 256 columns per block
   const int rows4 = (B + 3) / 4;
-  int nblk = (2 * 148 + rows4 - 1) / rows4;
+  int nblk = std::max((V + 4095) / 4096, (2 * 148 + rows4 - 1) / rows4);
   nblk = std::max(1, std::min(nblk, (V + 255) / 256));
   const int vpb = ((V + nblk - 1) / nblk + 255) / 256 * 256;
   return (V + vpb - 1) / vpb;

@@ -137,6 +137,61 @@ def scores_from_logits(logits, *, seed: int, step: int, rows=None, bias=None, te
     return Scores(rows=rows, v_global=v_global, ltilde=lt, g=g, s=lt + g)
 
 
+@dataclasses.dataclass
+class TopKResult:
+    idx: np.ndarray           # [R] sampled global id (-1: no finite l~)
+    s1: np.ndarray            # [R] winning perturbed score over the kept set
+    gap: np.ndarray           # [R] s1 - second best over the kept set (inf if one survivor)
+    kept: list                # per row: global ids of the kept set (top-k, then top-p), sorted
+    kth_margin: np.ndarray    # [R] l~ gap at the top-k boundary (rank k vs k+1; inf if none)
+    p_margin: np.ndarray      # [R] |cumsum before the top-p cut - p| (decision margin)
+
+
+def topk_topp_sample(sc: Scores, top_k: int, top_p: float = 1.0) -> TopKResult:
+    """Top-k then top-p (nucleus) sampling, exactly (§4.6; reading R19):
+      1. rank tokens by l~ descending, ties by smaller id; keep the first k with finite l~;
+      2. q = softmax of l~ over those k (fp64); keep the shortest prefix whose cumulative q >= p;
+      3. idx = argmax over the kept set of l~ + g (the same per-token Gumbels as the flat
+         sampler; Gumbel-max restricted to a subset samples the renormalised subset exactly)."""
+    R, V = sc.s.shape
+    idx = np.full(R, -1, np.int64)
+    s1 = np.full(R, -np.inf)
+    gap = np.full(R, np.inf)
+    kth = np.full(R, np.inf)
+    pm = np.full(R, np.inf)
+    kept_all = []
+    for r in range(R):
+        lt = sc.ltilde[r]
+        order = np.lexsort((sc.v_global, -lt))               # l~ desc, id asc
+        k = min(int(top_k), V)
+        cand = order[:k]
+        if k < V:
+            kth[r] = lt[order[k - 1]] - lt[order[k]]
+        cand = cand[np.isfinite(lt[cand])]
+        if cand.size == 0:
+            kept_all.append([])
+            continue
+        q = np.exp(lt[cand] - lt[cand[0]])
+        q = q / q.sum()
+        c = np.cumsum(q)
+        m = int(np.searchsorted(c, top_p, side="left")) if top_p < 1.0 else cand.size - 1
+        m = min(m, cand.size - 1)
+        keep = cand[:m + 1]
+        if top_p < 1.0:
+            before = c[m - 1] if m > 0 else 0.0
+            pm[r] = min(abs(c[m] - top_p), abs(before - top_p))
+        s = lt[keep] + sc.g[r, keep]
+        best = s.max()
+        win = keep[s == best]
+        j = win[np.argmin(sc.v_global[win])]
+        idx[r] = sc.v_global[j]
+        s1[r] = best
+        rest = s[keep != j]
+        gap[r] = best - rest.max() if rest.size else np.inf
+        kept_all.append(sorted(int(sc.v_global[x]) for x in keep))
+    return TopKResult(idx=idx, s1=s1, gap=gap, kept=kept_all, kth_margin=kth, p_margin=pm)
+
+
 def log_prob(sc: Scores, res: "FlatResult") -> np.ndarray:
     """log p(idx) = l~_idx - logsumexp(l~)  (App. E P:882: log-normalizer -> log-probabilities);
     -inf for undefined rows."""

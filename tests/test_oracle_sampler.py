@@ -306,3 +306,40 @@ def test_per_request_chi_square():
                               want_near=False).idx
     _, p = stats.chi_square(np.bincount(idx, minlength=8), stats.softmax_probs(lt))
     assert p > 1e-3
+
+
+def test_topk_topp_special_cases_and_hand_example():
+    rs = np.random.default_rng(12)
+    h = rs.standard_normal((7, 16)).astype(np.float32)
+    W = rs.standard_normal((200, 16)).astype(np.float32)
+    sc = sampler.scores(h, W, seed=2, step=5)
+    flat = sampler.flat_sample(sc)
+    full = sampler.topk_topp_sample(sc, top_k=200, top_p=1.0)       # no truncation == flat
+    assert np.array_equal(full.idx, flat.idx) and np.array_equal(full.s1, flat.s1)
+    one = sampler.topk_topp_sample(sc, top_k=1)                      # k = 1 == greedy argmax of l~
+    assert np.array_equal(one.idx, np.argmax(sc.ltilde, axis=1))
+    # hand example: l~ = ln[1,2,3,4]; k=4, p=0.5: sorted q = [.4,.3,.2,.1], cumsum .4,.7 -> keep {3,2}
+    lt = np.log(np.array([[1.0, 2.0, 3.0, 4.0]] * 16))
+    sc2 = sampler.scores_from_logits(lt, seed=1, step=0)
+    res = sampler.topk_topp_sample(sc2, top_k=4, top_p=0.5)
+    assert all(k == [2, 3] for k in res.kept) and set(res.idx.tolist()) <= {2, 3}
+    res = sampler.topk_topp_sample(sc2, top_k=2, top_p=1.0)
+    assert all(k == [2, 3] for k in res.kept)
+
+
+def test_topk_topp_chi_square():
+    # truncated, renormalised target: V=8 fixture, k=5, p=0.8
+    lt = np.array([0.5, -1.0, 2.0, 0.0, 1.5, -0.5, 1.0, 0.25])
+    order = np.lexsort((np.arange(8), -lt))[:5]
+    q = np.exp(lt[order] - lt[order].max()); q /= q.sum()
+    m = int(np.searchsorted(np.cumsum(q), 0.8))
+    keep = order[:m + 1]
+    target = np.zeros(8)
+    target[keep] = stats.softmax_probs(lt[keep])
+    n = 100_000
+    sc = sampler.scores_from_logits(np.tile(lt, (n, 1)), seed=31, step=0)
+    res = sampler.topk_topp_sample(sc, top_k=5, top_p=0.8)
+    counts = np.bincount(res.idx, minlength=8)
+    assert counts[np.setdiff1d(np.arange(8), keep)].sum() == 0
+    _, p = stats.chi_square(counts, target)
+    assert p > 1e-3

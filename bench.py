@@ -428,7 +428,12 @@ def sweep(fs, name, pk, args, Bs=(1, 8, 32, 128, 256)):
                 sctr[0] += 1
                 fs.sample_logits(lg, bias=wl["bias"], temperature=wl["temperature"], mask=wl["mask"],
                                  seed=synth.SAMPLING_SEED, step=sctr[0])
+            def ours_topk():
+                sctr[0] += 1
+                fs.sample_logits(lg, bias=wl["bias"], temperature=wl["temperature"], mask=wl["mask"],
+                                 seed=synth.SAMPLING_SEED, step=sctr[0], top_k=50, top_p=0.95)
             st = {"fs_sample_logits_us": round(1e3 * time_median(ours_sl, 100, 25), 2),
+                  "fs_sample_logits_top_k50_top_p095_us": round(1e3 * time_median(ours_topk, 100, 25), 2),
                   "logits_bytes": lg.numel() * 4}
             st["fs_sample_logits_gbs"] = round(st["logits_bytes"] / (st["fs_sample_logits_us"] * 1e-6) / 1e9, 1)
             try:
@@ -436,6 +441,8 @@ def sweep(fs, name, pk, args, Bs=(1, 8, 32, 128, 256)):
                 if wl["bias"] is None:
                     st["flashinfer_sampling_from_logits_us"] = round(
                         1e3 * time_median(lambda: fis.sampling_from_logits(lg), 100, 25), 2)
+                    st["flashinfer_top_k_top_p_k50_p095_us"] = round(
+                        1e3 * time_median(lambda: fis.top_k_top_p_sampling_from_logits(lg, 50, 0.95), 100, 25), 2)
             except Exception as e:  # pragma: no cover
                 st["flashinfer_error"] = repr(e)[:200]
             r["standalone_logits"] = st

@@ -156,13 +156,20 @@ typedef struct {
   float* logZ_out;           /* [B] or NULL */
   float* logprob_out;        /* [B] or NULL */
   fs_summary* groups_out;    /* [B][ceil(V/group_size)] or NULL (group_size > 0) */
+  int top_k;                 /* fs_sample_logits_ex: 1..1024 keeps the k largest l~ (R19); <= 0 off */
+  float top_p;               /* fs_sample_logits_ex: nucleus on the top-k survivors, (0,1); outside off */
 } fs_sample_args;
 
 /* fs_sample_ex -- fs_sample / fs_sample_grouped with per-request streams, greedy rows and every
  * optional output selected through `args` (same kernels, same conventions). */
 fs_status fs_sample_ex(fs_ctx* ctx, fs_dtype dtype, const void* h, const void* W, int B, int D, int V,
                        const fs_sample_args* args, void* stream);
-/* fs_sample_logits_ex -- fs_sample_logits with `args` (group_size and groups_out ignored). */
+/* fs_sample_logits_ex -- fs_sample_logits with `args` (group_size and groups_out ignored).
+ * Top-k / top-p (reading R19): with top_k in 1..1024 (required when
+ * 0 < top_p < 1) the sample is drawn exactly from softmax(l~) restricted to the k largest l~
+ * (ties -> smaller id) and then to the shortest prefix of those whose probability mass reaches
+ * top_p; logZ_out / logprob_out then refer to that truncated distribution.  Per-chunk top-k
+ * selection (block radix select) + per-row merge, top-p and Gumbel-max over the survivors. */
 fs_status fs_sample_logits_ex(fs_ctx* ctx, fs_dtype dtype, const void* logits, int64_t ld, int B, int V,
                               const fs_sample_args* args, void* stream);
 

@@ -165,7 +165,7 @@ def topk_topp_sample(sc: Scores, top_k: int, top_p: float = 1.0) -> TopKResult:
         order = np.lexsort((sc.v_global, -lt))               # l~ desc, id asc
         k = min(int(top_k), V)
         cand = order[:k]
-        if k < V:
+        if k < V and np.isfinite(lt[order[k - 1]]):
             kth[r] = lt[order[k - 1]] - lt[order[k]]
         cand = cand[np.isfinite(lt[cand])]
         if cand.size == 0:

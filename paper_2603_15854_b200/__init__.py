@@ -169,9 +169,10 @@ def sample_grouped(h, W, *, group_size: int, bias=None, temperature=None, mask=N
 
 
 def sample_logits(logits, *, bias=None, temperature=None, mask=None, seed: int = 0, step: int = 0,
-                  seeds=None, steps=None, return_all: bool = False):
+                  seeds=None, steps=None, top_k: int = 0, top_p: float = 1.0, return_all: bool = False):
     """Standalone Gumbel-max over materialised logits [B, V] (bf16 or fp32, row stride may exceed V)
-    (fs_sample_logits[_ex]).  Returns idx [B], or (idx, score, logZ, logprob) if return_all."""
+    (fs_sample_logits[_ex]).  top_k (1..1024) / top_p: exact top-k then nucleus sampling (R19).
+    Returns idx [B], or (idx, score, logZ, logprob) if return_all."""
     if not logits.is_cuda or logits.dim() != 2 or logits.stride(1) != 1:
         raise ValueError("logits must be a 2-D CUDA tensor with unit column stride")
     B, V = logits.shape
@@ -192,7 +193,8 @@ def sample_logits(logits, *, bias=None, temperature=None, mask=None, seed: int =
     logZ = torch.empty(B, dtype=torch.float32, device=dev) if return_all else None
     logprob = torch.empty(B, dtype=torch.float32, device=dev) if return_all else None
     args = _lib.SampleArgs(_ptr(bias), _ptr(temperature), _ptr(mask), seed & (2**64 - 1), step & (2**64 - 1),
-                           _ptr(seeds), _ptr(steps), 0, _ptr(idx), _ptr(score), _ptr(logZ), _ptr(logprob), None)
+                           _ptr(seeds), _ptr(steps), 0, _ptr(idx), _ptr(score), _ptr(logZ), _ptr(logprob), None,
+                           int(top_k), float(top_p))
     _lib.check(_lib.lib().fs_sample_logits_ex(context(dev), code, _ptr(logits), logits.stride(0), B, V,
                                               ctypes.byref(args), _stream(logits)), "fs_sample_logits_ex")
     return (idx, score, logZ, logprob) if return_all else idx

@@ -28,7 +28,7 @@ class SampleArgs(ctypes.Structure):
                 ("seed", ctypes.c_uint64), ("step", ctypes.c_uint64), ("seeds", ctypes.c_void_p),
                 ("steps", ctypes.c_void_p), ("group_size", ctypes.c_int), ("idx_out", ctypes.c_void_p),
                 ("score_out", ctypes.c_void_p), ("logZ_out", ctypes.c_void_p), ("logprob_out", ctypes.c_void_p),
-                ("groups_out", ctypes.c_void_p)]
+                ("groups_out", ctypes.c_void_p), ("top_k", ctypes.c_int), ("top_p", ctypes.c_float)]
 FS_BF16, FS_F32 = 0, 1
 
 

@@ -485,6 +485,25 @@ fs_status fs_sample_logits(fs_ctx* ctx, fs_dtype dtype, const void* logits, int6
 fs_status fs_sample_logits_ex(fs_ctx* ctx, fs_dtype dtype, const void* logits, int64_t ld, int B, int V,
                               const fs_sample_args* a, void* stream) {
   if (!a) return fail(FS_ERR_INVALID, "args is NULL");
+  const bool use_p = a->top_p > 0.0f && a->top_p < 1.0f;
+  if (a->top_k > 0 || use_p) {
+    if (a->top_k < 1 || a->top_k > fs::topk_max_k())
+      return fail(FS_ERR_UNSUPPORTED, "top-k sampling needs 1 <= top_k <= 1024 (also required for top_p)");
+    if (!ctx) return fail(FS_ERR_INVALID, "ctx is NULL");
+    if (dtype != FS_BF16 && dtype != FS_F32) return fail(FS_ERR_INVALID, "unknown dtype");
+    if (!logits || !a->idx_out) return fail(FS_ERR_INVALID, "logits and idx_out are required");
+    if (B < 1 || V < 1 || ld < V) return fail(FS_ERR_INVALID, "need B >= 1, V >= 1, ld >= V");
+    if (a->steps && !a->seeds) return fail(FS_ERR_INVALID, "steps requires seeds");
+    cudaError_t e = cudaSetDevice(ctx->device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    fs_status st = ensure_ws(ctx, (size_t)B * fs::topk_chunks(V) * a->top_k * 8);
+    if (st != FS_OK) return st;
+    e = fs::launch_topk_sample(dtype, logits, ld, a->bias, a->temperature, a->mask, ((int64_t)V + 31) / 32, B, V,
+                               a->top_k, use_p ? a->top_p : 1.0f, a->seed, a->step, a->seeds, a->steps, ctx->ws,
+                               a->idx_out, a->score_out, a->logZ_out, a->logprob_out,
+                               static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? FS_OK : cuda_fail(e, "top-k sampler launch");
+  }
   return sample_logits_impl(ctx, dtype, logits, ld, a->bias, a->temperature, a->mask, a->seed, a->step, a->seeds,
                             a->steps, B, V, a->idx_out, a->score_out, a->logZ_out, a->logprob_out, stream);
 }
@@ -492,6 +511,8 @@ fs_status fs_sample_logits_ex(fs_ctx* ctx, fs_dtype dtype, const void* logits, i
 fs_status fs_sample_ex(fs_ctx* ctx, fs_dtype dtype, const void* h, const void* W, int B, int D, int V,
                        const fs_sample_args* args, void* stream) {
   if (!args) return fail(FS_ERR_INVALID, "args is NULL");
+  if (args->top_k > 0 || (args->top_p > 0.0f && args->top_p < 1.0f))
+    return fail(FS_ERR_UNSUPPORTED, "top-k / top-p is implemented for materialised logits (fs_sample_logits_ex)");
   fs_status s = check_common(ctx, dtype, h, W, B, D, V);
   if (s != FS_OK) return s;
   if (!args->idx_out) return fail(FS_ERR_INVALID, "idx_out is required");

@@ -76,6 +76,15 @@ cudaError_t launch_logits_sample(fs_dtype dtype, const void* logits, int64_t ld,
                                  cudaStream_t stream, const uint64_t* seeds = nullptr,
                                  const uint64_t* steps = nullptr);
 int logits_sample_blocks(int B, int V);   // V blocks of the standalone sampler grid
+// Top-k / top-p over materialised logits: chunk candidates (workspace B*topk_chunks(V)*k*8 bytes)
+// then a per-row merge + top-p + Gumbel-max.
+int topk_chunks(int V);
+int topk_max_k();
+cudaError_t launch_topk_sample(fs_dtype dtype, const void* logits, int64_t ld, const float* bias,
+                               const float* temperature, const uint32_t* mask, int64_t mask_words, int B, int V,
+                               int k, float top_p, uint64_t seed, uint64_t step, const uint64_t* seeds,
+                               const uint64_t* steps, void* cand_ws, int32_t* idx_out, float* score_out,
+                               float* logZ_out, float* logprob_out, cudaStream_t stream);
 cudaError_t launch_combine(const fs_summary* gathered, int n, int B, int32_t* idx_out, float* score_out,
                            float* logZ_out, cudaStream_t stream);
 cudaError_t launch_merge(const fs_summary* a, const fs_summary* b, fs_summary* out, int count,

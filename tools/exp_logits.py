@@ -17,3 +17,12 @@ for B in (1, 32, 128, 256):
     t2 = bench.time_median(lambda: fis.sampling_from_logits(lg), 100, 25) * 1e3
     t3 = bench.time_median(seeds_, 100, 25) * 1e3
     print(f"B={B:4d} fs_sample_logits {t:8.2f} us ({lg.numel()*4/(t*1e-6)/1e9:7.1f} GB/s)  per-request {t3:8.2f}  flashinfer {t2:8.2f} us")
+for B in (1, 32, 128, 256):
+    lg = torch.randn(B, 128256, device=dev) * 1.3
+    ctr = [0]
+    def ours():
+        ctr[0] += 1
+        fs.sample_logits(lg, seed=1, step=ctr[0], top_k=50, top_p=0.95)
+    t = bench.time_median(ours, 100, 25) * 1e3
+    t2 = bench.time_median(lambda: fis.top_k_top_p_sampling_from_logits(lg, 50, 0.95), 100, 25) * 1e3
+    print(f"B={B:4d} top-k 50 / top-p 0.95: fs {t:8.2f} us   flashinfer {t2:8.2f} us")

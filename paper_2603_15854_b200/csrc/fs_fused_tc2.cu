@@ -74,6 +74,7 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
   if (XFORM) fill_rowtab<PRQ>(tab, p.B, p.temperature, p.seeds, p.steps, p.step, threadIdx.x, kThreads);
   sm100::tc_fence_before();
   sm100::cluster_sync();                    // both CTAs' barriers exist before any remote signal
+  __syncthreads();                          // CTA-level order for the allocator's smem write (racecheck)
   sm100::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   sm100::pdl_launch_dependents();

@@ -1,0 +1,32 @@
+"""Small invocations of every kernel for compute-sanitizer (memcheck / racecheck / synccheck)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import synth
+import paper_2603_15854_b200 as fs
+dev = "cuda"
+wl = synth.make_workload("qwen25_7b", 40, V=3000, D=136, with_transforms=True)
+h, W, bias, tau, mask = (x.to(dev) for x in (wl.h, wl.W, wl.bias, wl.temperature, wl.mask))
+for pair in (0, 1):
+    fs.set_option("pair", pair)
+    fs.sample(h, W, seed=1, step=2)
+    fs.sample(h, W, bias=bias, temperature=tau, mask=mask, seed=1, step=2, return_score=True)
+    fs.sample_grouped(h, W, group_size=512, bias=bias, temperature=tau, mask=mask, seed=1, step=2)
+    fs.sample(h, W, seeds=torch.arange(40, device=dev), step=3, return_logprob=True)
+    parts = [fs.sample_shard(h, W[a:b].contiguous(), a, 3000, seed=1, step=2).raw for a, b in ((0, 1500), (1500, 3000))]
+    fs.combine_summaries(torch.stack(parts))
+fs.set_option("pair", -1)
+fs.set_option("force_simt", 1)
+fs.sample(h, W, bias=bias, temperature=tau, mask=mask, seed=1, step=2)
+fs.set_option("force_simt", 0)
+tiny = synth.make_workload("tiny", 4)
+fs.sample(tiny.h.to(dev), tiny.W.to(dev), seed=1, step=0)
+lg = (h.float() @ W.float().t())
+fs.sample_logits(lg, bias=bias, temperature=tau, mask=mask, seed=1, step=1, return_all=True)
+fs.sample_logits(lg, top_k=20, top_p=0.9, seed=1, step=1, return_all=True)
+g = fs.sample_grouped(h, W, group_size=512, seed=1, step=0)[3]
+fs.merge_summaries(fs.Summaries(g.raw[:, 0].contiguous()), fs.Summaries(g.raw[:, 1].contiguous()))
+fs.gumbel_from_bits(torch.arange(1000, dtype=torch.int32, device=dev))
+fs.random_bits(1, 2, torch.arange(100, device=dev), torch.arange(100, device=dev))
+torch.cuda.synchronize()
+print("sanitize cases ok")

@@ -416,8 +416,13 @@ def sweep(fs, name, pk, args, Bs=(1, 8, 32, 128, 256)):
             def with_logprob():
                 vctr[0] += 1
                 fs.sample(wl["h"], wl["W"], seed=synth.SAMPLING_SEED, step=vctr[0], return_logprob=True)
+            def topk_fused():
+                vctr[0] += 1
+                fs.sample(wl["h"], wl["W"], seed=synth.SAMPLING_SEED, step=vctr[0], top_k=50, top_p=0.95, out=out)
             r["variants"] = {"per_request_seeds_us": round(1e3 * time_median(per_request, 100, 25), 2),
-                             "with_logZ_logprob_us": round(1e3 * time_median(with_logprob, 100, 25), 2)}
+                             "with_logZ_logprob_us": round(1e3 * time_median(with_logprob, 100, 25), 2),
+                             # SURVEY f1 through the LM head (vs baselines.fi1_gemm_top_k_top_p_us)
+                             "top_k50_top_p095_fused_us": round(1e3 * time_median(topk_fused, 100, 25), 2)}
         if not args.no_baselines and not wl["group_size"]:
             # standalone sampling over the same materialised fp32 logits (§5.2):
             # fs_sample_logits vs FlashInfer's Gumbel-max sampling_from_logits (FI2's sampler)

@@ -156,12 +156,20 @@ typedef struct {
   float* logZ_out;           /* [B] or NULL */
   float* logprob_out;        /* [B] or NULL */
   fs_summary* groups_out;    /* [B][ceil(V/group_size)] or NULL (group_size > 0) */
-  int top_k;                 /* fs_sample_logits_ex: 1..1024 keeps the k largest l~ (R19); <= 0 off */
-  float top_p;               /* fs_sample_logits_ex: nucleus on the top-k survivors, (0,1); outside off */
+  int top_k;                 /* 1..1024 keeps the k largest l~ (R19); <= 0 off */
+  float top_p;               /* nucleus on the top-k survivors, (0,1); outside off */
 } fs_sample_args;
 
 /* fs_sample_ex -- fs_sample / fs_sample_grouped with per-request streams, greedy rows and every
- * optional output selected through `args` (same kernels, same conventions). */
+ * optional output selected through `args` (same kernels, same conventions).
+ * With top_k / top_p ("each tile computes top-k candidates locally,
+ * a second stage reduces all per-tile candidates into a global top-k"; reading R19): the same
+ * truncated distribution as fs_sample_logits_ex, through the LM head.  Stage 1 keeps the k best
+ * (l~, id) per (row, CTA) in the epilogue's shared memory (logits never reach HBM); when those
+ * lists do not fit (large B x k) it writes the fp32 logits to the context workspace instead
+ * (B x V x 4 bytes) and the chunked selection of fs_sample_logits_ex runs on them -- same
+ * accumulator, same transform, same token.  FS_ERR_UNSUPPORTED with grouped outputs
+ * (group_size < V or groups_out). */
 fs_status fs_sample_ex(fs_ctx* ctx, fs_dtype dtype, const void* h, const void* W, int B, int D, int V,
                        const fs_sample_args* args, void* stream);
 /* fs_sample_logits_ex -- fs_sample_logits with `args` (group_size and groups_out ignored).

@@ -101,17 +101,19 @@ def _u64(t, B, name, dev):
 
 
 def sample(h, W, *, bias=None, temperature=None, mask=None, seed: int = 0, step: int = 0,
-           seeds=None, steps=None, return_score: bool = False, return_logprob: bool = False, out=None):
+           seeds=None, steps=None, top_k: int = 0, top_p: float = 1.0, return_score: bool = False,
+           return_logprob: bool = False, out=None):
     """Fused LM-head + exact Gumbel-max sample per row.  Returns int32 [B]; with return_score
     also the winning perturbed scores; with return_logprob also (logZ, log p(idx)).
     seeds / steps: optional [B] int64 per-request streams (batch-position invariant, reading R18);
-    temperature[b] == 0 samples row b greedily."""
+    temperature[b] == 0 samples row b greedily.  top_k (1..1024) / top_p: exact top-k then
+    nucleus sampling through the LM head (reading R19; logZ / log-prob are those of the kept set)."""
     B, D, V = _check_inputs(h, W, bias, temperature, mask)
     idx = out if out is not None else torch.empty(B, dtype=torch.int32, device=h.device)
     score = torch.empty(B, dtype=torch.float32, device=h.device) if return_score else None
     seeds = _u64(seeds, B, "seeds", h.device)
     steps = _u64(steps, B, "steps", h.device)
-    if seeds is None and steps is None and not return_logprob:
+    if seeds is None and steps is None and not return_logprob and not top_k and top_p >= 1.0:
         _lib.check(_lib.lib().fs_sample(context(h.device), _dtype_code(h, W), _ptr(h), _ptr(W), _ptr(bias),
                                         _ptr(temperature), _ptr(mask), seed & (2**64 - 1), step & (2**64 - 1),
                                         B, D, V, _ptr(idx), _ptr(score), _stream(h)), "fs_sample")
@@ -119,7 +121,8 @@ def sample(h, W, *, bias=None, temperature=None, mask=None, seed: int = 0, step:
     logZ = torch.empty(B, dtype=torch.float32, device=h.device) if return_logprob else None
     logprob = torch.empty(B, dtype=torch.float32, device=h.device) if return_logprob else None
     args = _lib.SampleArgs(_ptr(bias), _ptr(temperature), _ptr(mask), seed & (2**64 - 1), step & (2**64 - 1),
-                           _ptr(seeds), _ptr(steps), 0, _ptr(idx), _ptr(score), _ptr(logZ), _ptr(logprob), None)
+                           _ptr(seeds), _ptr(steps), 0, _ptr(idx), _ptr(score), _ptr(logZ), _ptr(logprob), None,
+                           int(top_k), float(top_p))
     _lib.check(_lib.lib().fs_sample_ex(context(h.device), _dtype_code(h, W), _ptr(h), _ptr(W), B, D, V,
                                        ctypes.byref(args), _stream(h)), "fs_sample_ex")
     res = (idx,) + ((score,) if return_score else ()) + ((logZ, logprob) if return_logprob else ())

@@ -51,6 +51,8 @@ struct fs_ctx {
   int unit_rows = 0;               // CTA range granularity (0 = default)
   int pair = -1;                   // CTA-pair kernel: -1 auto (by batch size), 0 off, 1 on
   int pair_min_bn = 32;            // auto: use the pair kernel from this MMA N upwards (measured)
+  int topk_mode = 0;               // fused top-k: 0 auto, 1 candidate lists in the epilogue, 2 via raw logits
+  int* topk_rowcnt = nullptr;      // [256] per-row candidate counters of the list route (kept at 0 between calls)
   // tensor-map cache: encoding costs host microseconds per map; W maps are reused across calls
   struct MapKey { const void* base; int64_t inner, rows; int box, promo; };
   struct MapEnt { MapKey k; CUtensorMap m; };
@@ -182,6 +184,22 @@ struct PathArgs {
   const uint64_t* steps = nullptr;
 };
 
+// time_stage1 option: record a start event now and return the end event to record after stage 1.
+fs_status stage1_event(fs_ctx* ctx, cudaStream_t stream, cudaEvent_t* ev_end) {
+  *ev_end = nullptr;
+  if (!ctx->time_stage1) return FS_OK;
+  if (ctx->ev_used == ctx->ev_pool.size()) {
+    cudaEvent_t e0, e1;
+    if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess)
+      return fail(FS_ERR_CUDA, "cudaEventCreate");
+    ctx->ev_pool.emplace_back(e0, e1);
+  }
+  cudaEventRecord(ctx->ev_pool[ctx->ev_used].first, stream);
+  *ev_end = ctx->ev_pool[ctx->ev_used].second;
+  ++ctx->ev_used;
+  return FS_OK;
+}
+
 fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
   cudaError_t e = cudaSetDevice(ctx->device);
   if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
@@ -238,17 +256,7 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
     p.part = part;
     p.part_group = part_group;
     cudaEvent_t ev_end = nullptr;
-    if (ctx->time_stage1) {
-      if (ctx->ev_used == ctx->ev_pool.size()) {
-        cudaEvent_t e0, e1;
-        if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess)
-          return fail(FS_ERR_CUDA, "cudaEventCreate");
-        ctx->ev_pool.emplace_back(e0, e1);
-      }
-      cudaEventRecord(ctx->ev_pool[ctx->ev_used].first, stream);
-      ev_end = ctx->ev_pool[ctx->ev_used].second;
-      ++ctx->ev_used;
-    }
+    if ((st = stage1_event(ctx, stream, &ev_end)) != FS_OK) return st;
     if (tc) {
       const int BN = fs::tc_block_n(Bc);
       // K slices per TMA stage: as many as keep >= 3 stages in flight (more contiguous bytes per
@@ -286,6 +294,143 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
                           a.groups_out ? a.groups_out + (size_t)r0 * a.n_groups : nullptr, stream,
                           ctx->pdl != 0 && !ctx->time_stage1, a.logprob_out ? a.logprob_out + r0 : nullptr);
     if (e != cudaSuccess) return cuda_fail(e, "stage-2 reduce launch");
+  }
+  return FS_OK;
+}
+
+// Top-k / top-p through the LM head (reading R19).  Stage 1 either keeps the
+// k best (key(l~), id) per (row, CTA) in the epilogue (mode 1: logits never leave the SM) or,
+// when those lists do not fit in shared memory, stores the raw fp32 logits (mode 2) for the
+// chunked top-k kernels.  Both routes see the same fp32 accumulator and transform, so they pick
+// the same token.  Stage 2 = topk_final_kernel (merge, top-p, Gumbel-max over the kept set).
+fs_status run_topk_path(fs_ctx* ctx, const PathArgs& a, int k, float top_p, cudaStream_t stream) {
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  const bool tc = !ctx->force_simt && a.dtype == FS_BF16 && (a.D % 8 == 0) && aligned16(a.h) && aligned16(a.W);
+  const size_t esz = a.dtype == FS_BF16 ? 2 : 4;
+  const int unit = ctx->unit_rows > 0 ? ctx->unit_rows : 16;
+  const int U = (a.V + unit - 1) / unit;
+  const int G = std::min(std::max(1, ctx->max_ctas > 0 ? ctx->max_ctas : ctx->num_sms), U);
+  const int chunk = 256;
+  const int Bc_max = std::min(a.B, chunk);
+  const int BN_max = fs::tc_block_n(Bc_max);
+  const int cap = ((k + 31) / 32) * 32 + 128;
+  const int extra = fs::tc_topk_extra_bytes(BN_max, cap);
+  // lists only when the TMA ring keeps >= 8 K-slices (128 KB of W) in flight next to them
+  // (fewer starve the HBM stream; measured: B=64, k=50 -> 4 slices, 356 vs 166 us stage 1)
+  auto ring_slices = [&](int BN, int ex) {
+    int best = 0;
+    for (int kk = 1; kk <= 4; ++kk) {
+      const int S = fs::tc_stages(BN, kk, ex);
+      if (S >= 2) best = std::max(best, kk * S);
+    }
+    return best;
+  };
+  const int slices = tc ? ring_slices(BN_max, extra) : 0;
+  if (ctx->topk_mode == 1 && slices < 2)
+    return fail(FS_ERR_UNSUPPORTED, "top-k candidate lists do not fit in shared memory for this B and k (topk_mode=1)");
+  // auto: lists for k <= 128 when the ring keeps >= 8 slices (measured: at k = 200 the
+  // per-tile compactions cost more than the raw-logit round trip)
+  const bool lists = ctx->topk_mode == 1 || (ctx->topk_mode == 0 && slices >= 8 && k <= 128);
+  if (lists && !ctx->topk_rowcnt) {
+    e = cudaMalloc(&ctx->topk_rowcnt, 256 * sizeof(int));
+    if (e != cudaSuccess) return fail(FS_ERR_OOM, "row counter cudaMalloc failed");
+    e = cudaMemset(ctx->topk_rowcnt, 0, 256 * sizeof(int));
+    if (e != cudaSuccess) return cuda_fail(e, "row counter memset");
+  }
+  const CUtensorMap* wmaps = nullptr;
+  int max_seg = 1;
+  if (tc) {
+    fs_status st0 = segment_maps(ctx, a.W, a.D, a.V, G, unit, a.V, &wmaps, &max_seg);
+    if (st0 != FS_OK) return st0;
+  }
+  // workspace: candidates [Bc][G*k] (lists) or logits [Bc][V] fp32 + chunk candidates
+  const int nslot = lists ? G : fs::topk_chunks(a.V);
+  const int stride = lists ? G * cap : nslot * k;            // candidates per row
+  const size_t cand_bytes = (size_t)Bc_max * (stride * sizeof(fs::Cand) + nslot * sizeof(uint32_t));
+  const size_t mat_off = (cand_bytes + 255) & ~size_t(255);
+  const size_t mat_bytes = lists ? 0 : (size_t)Bc_max * a.V * sizeof(float);
+  fs_status st = ensure_ws(ctx, mat_off + mat_bytes);
+  if (st != FS_OK) return st;
+  fs::Cand* cand = static_cast<fs::Cand*>(ctx->ws);
+  float* mat = reinterpret_cast<float*>(static_cast<char*>(ctx->ws) + mat_off);
+  for (int r0 = 0; r0 < a.B; r0 += chunk) {
+    const int Bc = std::min(chunk, a.B - r0);
+    fs::StageOneParams p{};
+    p.h = static_cast<const char*>(a.h) + (size_t)r0 * a.D * esz;
+    p.W = a.W;
+    p.bias = a.bias;
+    p.temperature = a.temperature ? a.temperature + r0 : nullptr;
+    p.mask = a.mask ? a.mask + (size_t)r0 * a.mask_words : nullptr;
+    p.mask_words = a.mask_words;
+    p.vocab_offset = a.vocab_offset;
+    p.seed = a.seed;
+    p.step = a.step;
+    p.B = Bc;
+    p.D = a.D;
+    p.V = a.V;
+    p.row_offset = r0;
+    p.group_size = ((a.V + 127) / 128) * 128;
+    p.max_seg = max_seg;
+    p.unit_rows = unit;
+    p.mode = lists ? 1 : 2;
+    p.topk_k = k;
+    p.topk_cap = cap;
+    p.topk_cand = cand;
+    p.topk_stride = stride;
+    p.topk_rowcnt = ctx->topk_rowcnt;
+    p.topk_lb = reinterpret_cast<uint32_t*>(cand + (size_t)Bc * stride);
+    p.topk_m = (k + G - 1) / G;
+    p.mat_out = mat;
+    p.mat_ld = a.V;
+    cudaEvent_t ev_end = nullptr;
+    if ((st = stage1_event(ctx, stream, &ev_end)) != FS_OK) return st;
+    if (tc) {
+      const int BN = fs::tc_block_n(Bc);
+      p.w_policy = ctx->w_policy;
+      p.dbg_no_epi = ctx->dbg_no_epi;
+      p.dbg_no_mma = ctx->dbg_no_mma;
+      const int ex = lists ? fs::tc_topk_extra_bytes(BN, cap) : 0;
+      p.kbps = 0;
+      for (int kk = 4; kk >= 2; --kk)
+        if (fs::tc_stages(BN, kk, ex) >= 3) { p.kbps = kk; break; }
+      if (p.kbps == 0) {                      // no depth-3 ring: the most slices with >= 2 stages
+        int best = 0;
+        for (int kk = 1; kk <= 4; ++kk) {
+          const int S = fs::tc_stages(BN, kk, ex);
+          if (S >= 2 && kk * S > best) { best = kk * S; p.kbps = kk; }
+        }
+      }
+      if (p.kbps == 0) p.kbps = 1;
+      p.stages = fs::tc_stages(BN, p.kbps, ex);
+      if (p.stages < 2) return fail(FS_ERR_INVALID, "shared memory too small for the top-k epilogue");
+      CUtensorMap hmap;
+      if ((st = make_map(ctx, &hmap, p.h, a.D, Bc, BN)) != FS_OK) return st;
+      p.wmaps = wmaps;
+      e = fs::launch_fused_tc_topk(hmap, p, BN, G, stream);
+      if (e != cudaSuccess) return cuda_fail(e, "stage-1 top-k kernel launch");
+    } else {
+      e = fs::launch_fused_simt(p, a.dtype, false, stream);
+      if (e != cudaSuccess) return cuda_fail(e, "stage-1 CUDA-core logits kernel launch");
+    }
+    if (ev_end) cudaEventRecord(ev_end, stream);
+    int32_t* idx = a.idx_out + r0;
+    float* sc = a.score_out ? a.score_out + r0 : nullptr;
+    float* lz = a.logZ_out ? a.logZ_out + r0 : nullptr;
+    float* lp = a.logprob_out ? a.logprob_out + r0 : nullptr;
+    const uint64_t* sd = a.seeds ? a.seeds + r0 : nullptr;
+    const uint64_t* stp = a.steps ? a.steps + r0 : nullptr;
+    if (lists)
+      e = fs::launch_topk_final(cand, stride, ctx->topk_rowcnt, Bc, k, top_p, p.temperature, a.seed, a.step, sd, stp,
+                                idx, sc, lz, lp, stream, r0, ctx->pdl != 0 && !ctx->time_stage1, p.topk_lb, G,
+                                p.topk_m);
+    else
+      e = fs::launch_topk_sample(FS_F32, mat, a.V, a.bias, p.temperature, p.mask, a.mask_words, Bc, a.V, k, top_p,
+                                 a.seed, a.step, sd, stp, cand, idx, sc, lz, lp, stream, r0);
+    if (e != cudaSuccess) {
+      if (lists) cudaMemsetAsync(ctx->topk_rowcnt, 0, 256 * sizeof(int), stream);   // keep the counters valid
+      return cuda_fail(e, "top-k stage-2 launch");
+    }
   }
   return FS_OK;
 }
@@ -354,6 +499,7 @@ void fs_ctx_destroy(fs_ctx* ctx) {
     cudaEventDestroy(pr.second);
   }
   if (ctx->ws) cudaFree(ctx->ws);
+  if (ctx->topk_rowcnt) cudaFree(ctx->topk_rowcnt);
   delete ctx;
 }
 
@@ -371,6 +517,10 @@ fs_status fs_ctx_set_option(fs_ctx* ctx, const char* name, int64_t value) {
   else if (!strcmp(name, "epi_sleep")) ctx->epi_sleep = (int)value;
   else if (!strcmp(name, "pair")) ctx->pair = (int)value;
   else if (!strcmp(name, "pair_min_bn")) ctx->pair_min_bn = (int)value;
+  else if (!strcmp(name, "topk_mode")) {
+    if (value < 0 || value > 2) return fail(FS_ERR_INVALID, "topk_mode must be 0 (auto), 1 (epilogue lists) or 2 (raw logits)");
+    ctx->topk_mode = (int)value;
+  }
   else if (!strcmp(name, "unit_rows")) {
     if (value != 0 && value != 16 && value != 32 && value != 64 && value != 128)
       return fail(FS_ERR_INVALID, "unit_rows must be 0, 16, 32, 64 or 128");
@@ -496,7 +646,7 @@ fs_status fs_sample_logits_ex(fs_ctx* ctx, fs_dtype dtype, const void* logits, i
     if (a->steps && !a->seeds) return fail(FS_ERR_INVALID, "steps requires seeds");
     cudaError_t e = cudaSetDevice(ctx->device);
     if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
-    fs_status st = ensure_ws(ctx, (size_t)B * fs::topk_chunks(V) * a->top_k * 8);
+    fs_status st = ensure_ws(ctx, (size_t)B * fs::topk_chunks(V) * (a->top_k * 8 + 4));
     if (st != FS_OK) return st;
     e = fs::launch_topk_sample(dtype, logits, ld, a->bias, a->temperature, a->mask, ((int64_t)V + 31) / 32, B, V,
                                a->top_k, use_p ? a->top_p : 1.0f, a->seed, a->step, a->seeds, a->steps, ctx->ws,
@@ -511,12 +661,21 @@ fs_status fs_sample_logits_ex(fs_ctx* ctx, fs_dtype dtype, const void* logits, i
 fs_status fs_sample_ex(fs_ctx* ctx, fs_dtype dtype, const void* h, const void* W, int B, int D, int V,
                        const fs_sample_args* args, void* stream) {
   if (!args) return fail(FS_ERR_INVALID, "args is NULL");
-  if (args->top_k > 0 || (args->top_p > 0.0f && args->top_p < 1.0f))
-    return fail(FS_ERR_UNSUPPORTED, "top-k / top-p is implemented for materialised logits (fs_sample_logits_ex)");
   fs_status s = check_common(ctx, dtype, h, W, B, D, V);
   if (s != FS_OK) return s;
   if (!args->idx_out) return fail(FS_ERR_INVALID, "idx_out is required");
   if (args->steps && !args->seeds) return fail(FS_ERR_INVALID, "steps requires seeds");
+  const bool use_p = args->top_p > 0.0f && args->top_p < 1.0f;
+  if (args->top_k > 0 || use_p) {
+    if (args->top_k < 1 || args->top_k > fs::topk_max_k())
+      return fail(FS_ERR_UNSUPPORTED, "top-k sampling needs 1 <= top_k <= 1024 (also required for top_p)");
+    if (args->groups_out || (args->group_size > 0 && args->group_size < V))
+      return fail(FS_ERR_UNSUPPORTED, "top-k / top-p has no grouped summaries");
+    PathArgs a{dtype, h, W, args->bias, args->temperature, args->mask, ((int64_t)V + 31) / 32, args->seed,
+               args->step, B, D, V, 0, V, false, args->idx_out, args->score_out, args->logZ_out, nullptr, 1,
+               args->logprob_out, args->seeds, args->steps};
+    return run_topk_path(ctx, a, args->top_k, use_p ? args->top_p : 1.0f, static_cast<cudaStream_t>(stream));
+  }
   int gs = args->group_size;
   if (gs < 0 || (gs > 0 && gs % 128 != 0)) return fail(FS_ERR_INVALID, "group_size must be 0 or a multiple of 128");
   if (gs == 0 || gs >= V) gs = ((V + 127) / 128) * 128;

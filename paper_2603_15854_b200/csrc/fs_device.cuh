@@ -123,6 +123,26 @@ __device__ __forceinline__ float key_ref(uint32_t key) {
   return key > kKeyNegInf ? key_to_float(key) : -INFINITY;
 }
 
+// Top-k candidate: order key of the transformed logit l~ and its global id.
+struct Cand {
+  uint32_t key;
+  int32_t idx;
+};
+
+// Histogram increment of bin d by every active lane of a converged warp.  Radix digits of the
+// top-k keys are highly concentrated (similar logits share sign, exponent and leading mantissa
+// bits), and same-address shared atomics serialise: the lanes that agree with the first active
+// lane's bin are folded into one atomic, the rest add individually.
+__device__ __forceinline__ void warp_hist_add(uint32_t* hist, bool act, uint32_t d, int lane) {
+  const uint32_t am = __ballot_sync(0xFFFFFFFFu, act);
+  if (am == 0u) return;
+  const int leader = __ffs(am) - 1;
+  const uint32_t dl = __shfl_sync(0xFFFFFFFFu, d, leader);
+  const uint32_t same = __ballot_sync(0xFFFFFFFFu, act && d == dl);
+  if (lane == leader) atomicAdd(&hist[dl], (uint32_t)__popc(same));
+  else if (act && d != dl) atomicAdd(&hist[d], 1u);
+}
+
 // Max-merge only (no log-mass): larger key wins, ties -> smaller id.
 __device__ __forceinline__ State state_max(State a, State b) {
   const bool take_b = (b.key > a.key) || (b.key == a.key && b.idx >= 0 && (a.idx < 0 || b.idx < a.idx));

@@ -64,8 +64,16 @@ __global__ void __launch_bounds__(128) fused_simt_kernel(const StageOneParams p)
       for (int j = 0; j < 32; ++j)
         if (j < nb) acc[j] = fmaf(ldf(h + (size_t)(c * 32 + j) * p.D + d), w, acc[j]);
     }
+    if (p.mode == 2) {                        // raw logits for the top-k fallback (f1)
+      if (ra.valid)
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < nb) p.mat_out[(int64_t)(c * 32 + j) * p.mat_ld + row] = acc[j];
+      continue;
+    }
     epi_columns<32, LSE, PRQ>(acc, c * 32, ra, ea, st[c], lane);
   }
+  if (p.mode == 2) return;
   flush_states<kSimtChunks, 32>(st, scratch, 256, q, lane, threadIdx.x, p.B, p.part + (size_t)blockIdx.x * p.B, 1);
   if (threadIdx.x == 0) p.part_group[blockIdx.x] = base / p.group_size;
   sm100::pdl_launch_dependents();

@@ -23,6 +23,7 @@
 
 #include "fs_epilogue.cuh"
 #include "fs_kernels.h"
+#include "fs_topk_epi.cuh"
 
 namespace fs {
 
@@ -43,11 +44,14 @@ static int tmem_cols_for(int BN) {
 // [a + 128k, min(b, a + 128(k+1))).
 __device__ __forceinline__ int seg_end(int a, int r1, int gs) { return min(r1, (a / gs + 1) * gs); }
 
-template <bool LSE, bool XFORM, bool PRQ>
+// MODE 0: sampling epilogue; 1: top-k candidate lists (fs_topk_epi.cuh); 2: raw fp32 logits.
+template <bool LSE, bool XFORM, bool PRQ, int MODE = 0>
 __global__ void __launch_bounds__(kThreadsTC, 1)
 fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned base by pointer arithmetic on the shared array, so that every pointer derived
+  // from it stays in the shared address space (LDS/STS/ATOMS, not generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
   const int S = p.stages, BN = p.bn, KBPS = p.kbps;
   const int h_stage_bytes = BN * kBlockK * 2;                 // per 64-wide K slice
   uint8_t* w_ring = smem;
@@ -59,6 +63,20 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   RowTab* tab = reinterpret_cast<RowTab*>(tmem_slot + 4);
   const CUtensorMap* wmaps = p.wmaps + (size_t)blockIdx.x * p.max_seg;
+  TopkSmem ts{};
+  if (MODE == 1) {
+    uint8_t* tk = reinterpret_cast<uint8_t*>(tab + 1);
+    ts.thr = reinterpret_cast<uint32_t*>(tk);
+    ts.cnt = reinterpret_cast<int*>(ts.thr + BN);
+    ts.hist = reinterpret_cast<uint32_t*>(ts.cnt + BN);
+    ts.buf = reinterpret_cast<Cand*>(ts.hist + kEpiWarps * 256);
+    ts.cap = p.topk_cap;
+    ts.k = p.topk_k;
+    for (int i = threadIdx.x; i < BN; i += kThreadsTC) {
+      ts.thr[i] = kKeyNegInf;                     // only finite l~ enter (R19)
+      ts.cnt[i] = 0;
+    }
+  }
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -70,7 +88,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
     }
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&tfull[i], 1);
-      sm100::mbar_init(&tempty[i], 128);
+      sm100::mbar_init(&tempty[i], MODE == 1 ? 256 : 128);   // mode 1: both warp quads drain every tile
     }
     sm100::fence_barrier_init();
   }
@@ -152,6 +170,66 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
         }
         a = b;
       }
+    }
+  } else if constexpr (MODE == 1) {
+    // ------------------------- top-k candidate epilogue (f1) ----------------------------
+    const int e = warp - 2;
+    const int qd = e >> 2, wq = e & 3, q = warp & 3;
+    EpiArgs ea{};
+    ea.invtau = tab->invtau;
+    ea.tab = tab;
+    ea.mask = p.mask;
+    ea.mask_words = p.mask_words;
+    ea.B = p.B;
+    uint32_t* hist = ts.hist + e * 256;
+    int tile_i = 0;
+    for (int a = r0; a < r1;) {
+      const int b = seg_end(a, r1, gs);
+      for (int t0 = a; t0 < b; t0 += kBlockM, ++tile_i) {
+        const int buf = tile_i & 1;
+        const uint32_t use = (uint32_t)(tile_i >> 1);
+        sm100::mbar_wait(&tfull[buf], use & 1);
+        sm100::tc_fence_after();
+        const int t1 = min(b, t0 + kBlockM);
+        const int row = t0 + 32 * q + lane;
+        RowArgs ra;
+        ra.valid = row < t1;
+        ra.v_global = (int32_t)(p.vocab_offset + row);
+        ra.v_lo = (uint32_t)ra.v_global;
+        ra.warp_v0 = (int32_t)(p.vocab_offset + t0 + 32 * q);
+        ra.bias = (XFORM && ra.valid && p.bias) ? p.bias[row] : 0.0f;
+        const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * BN);
+        if (p.dbg_no_epi == 0) epi_tile_topk<XFORM>(taddr, ra, ea, ts, lane, qd);
+        release_tmem(&tempty[buf], 0, lane);
+        if (p.dbg_no_epi < 2) {
+          sm100::named_bar_sync(2 + qd, 128);
+          topk_compact_cols(ts, p.B, qd, wq, ts.cap - kBlockM, hist, lane);   // room for one more tile
+          sm100::named_bar_sync(2 + qd, 128);
+        }
+      }
+      a = b;
+    }
+    topk_write_cols(ts, p.B, qd, wq, lane, p.topk_cand, p.topk_stride, p.topk_rowcnt, p.topk_lb, gridDim.x,
+                    blockIdx.x, p.topk_m, hist);
+  } else if constexpr (MODE == 2) {
+    // ------------------------------ raw logits (fallback) -------------------------------
+    const int e = warp - 2;
+    const int set = e >> 2;
+    const int q = warp & 3;
+    int tile_i = 0;
+    for (int a = r0; a < r1;) {
+      const int b = seg_end(a, r1, gs);
+      for (int t0 = a; t0 < b; t0 += kBlockM, ++tile_i) {
+        if ((tile_i & 1) != set) continue;
+        const uint32_t use = (uint32_t)(tile_i >> 1);
+        sm100::mbar_wait(&tfull[set], use & 1);
+        sm100::tc_fence_after();
+        const int row = t0 + 32 * q + lane;
+        const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(set * BN);
+        epi_tile_store(taddr, row < min(b, t0 + kBlockM), row, p.B, p.mat_out, p.mat_ld);
+        release_tmem(&tempty[set], 0, lane);
+      }
+      a = b;
     }
   } else {
     // -------------------------------- epilogue ------------------------------------------
@@ -248,15 +326,40 @@ int tc_block_n(int B) {
   return ((B + 31) / 32) * 32;
 }
 
-int tc_stages(int BN, int kbps) {
+int tc_stages(int BN, int kbps, int extra) {
   const int budget = 227 * 1024 - 1024;
   const int stage = (kWStageBytes + BN * kBlockK * 2) * kbps;
   int S = 16;
-  while (S > 0 && S * stage + kExtraBytes > budget) --S;
+  while (S > 0 && S * stage + kExtraBytes + extra > budget) --S;
   return S;
 }
 
+int tc_topk_extra_bytes(int BN, int cap) {
+  return 2 * BN * 4 + kEpiWarps * 256 * 4 + BN * cap * (int)sizeof(Cand) + 16;
+}
+
 int tc_slots_per_segment() { return kEpiWarps; }
+
+cudaError_t launch_fused_tc_topk(const CUtensorMap& hmap, const StageOneParams& p_in, int BN, int grid,
+                                 cudaStream_t stream) {
+  StageOneParams p = p_in;
+  p.bn = BN;
+  p.tmem_cols = tmem_cols_for(BN);
+  const int extra = p.mode == 1 ? tc_topk_extra_bytes(BN, p.topk_cap) : 0;
+  const size_t smem = 1024 + (size_t)p.stages * p.kbps * (kWStageBytes + BN * kBlockK * 2) + kExtraBytes + extra;
+  const bool xform = p.bias || p.temperature || p.mask;
+  auto kern = p.mode == 2 ? fused_tc_kernel<false, false, false, 2>
+                          : xform ? fused_tc_kernel<false, true, false, 1> : fused_tc_kernel<false, false, false, 1>;
+  static bool attr_set[3] = {false, false, false};
+  const int variant = p.mode == 2 ? 2 : xform ? 1 : 0;
+  if (!attr_set[variant]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr_set[variant] = true;
+  }
+  kern<<<grid, kThreadsTC, smem, stream>>>(hmap, p);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_fused_tc(const CUtensorMap& hmap, const StageOneParams& p_in, int BN, bool lse, int grid,
                             cudaStream_t stream) {

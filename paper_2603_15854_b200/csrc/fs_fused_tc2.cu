@@ -41,7 +41,9 @@ template <bool LSE, bool XFORM, bool PRQ>
 __global__ void __launch_bounds__(kThreads, 1)
 fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned base by pointer arithmetic on the shared array, so that every pointer derived
+  // from it stays in the shared address space (LDS/STS/ATOMS, not generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
   const int S = p.stages, BN = p.bn, KBPS = p.kbps;
   const int h_bytes = (BN / 2) * kBlockK * 2;                 // this CTA's half of h per K slice
   uint8_t* w_ring = smem;

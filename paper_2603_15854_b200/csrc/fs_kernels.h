@@ -9,6 +9,7 @@
 namespace fs {
 
 struct State;
+struct Cand;
 
 // Parameters of one stage-1 launch (one chunk of <= 256 batch rows).
 struct StageOneParams {
@@ -38,11 +39,22 @@ struct StageOneParams {
   const CUtensorMap* wmaps;   // [grid][max_seg] device TMA descriptors of each CTA segment (TC kernel)
   State* part;                // [grid * max_seg][B] candidate states
   int* part_group;            // [grid * max_seg] group id of each slot, -1 = unused
+  int mode;                   // 0 sample; 1 top-k candidates (fs_topk_epi.cuh); 2 store raw logits
+  int topk_k;                 // mode 1: k
+  int topk_cap;               // mode 1: candidate list capacity per column (>= k rounded to 32, + 128)
+  Cand* topk_cand;            // mode 1: [B][topk_stride] candidates, appended at topk_rowcnt[b] (atomic)
+  int topk_stride;            // mode 1: candidate capacity per row (grid * topk_cap)
+  int* topk_rowcnt;           // mode 1: [B] candidates written per row (zero on entry)
+  uint32_t* topk_lb;          // mode 1: [B][grid] each CTA's topk_m-th largest key (0 if fewer)
+  int topk_m;                 // mode 1: ceil(k / grid)
+  float* mat_out;             // mode 2: [B][mat_ld] fp32 logits of the local rows
+  int64_t mat_ld;
 };
 
 
 int tc_block_n(int B);
-int tc_stages(int BN, int kbps);
+int tc_stages(int BN, int kbps, int extra = 0);
+int tc_topk_extra_bytes(int BN, int cap);   // shared memory of the top-k lists (mode 1)
 int tc_slots_per_segment();   // candidate slots one CTA writes per group segment
 int tc2_stages(int BN, int kbps);
 // CTA-pair (cta_group::2) stage 1: grid = 2 x pairs, cluster (2,1,1); h map box = BN/2 rows.
@@ -50,6 +62,9 @@ cudaError_t launch_fused_tc2(const CUtensorMap& hmap, const StageOneParams& p, i
                              cudaStream_t stream);
 cudaError_t launch_fused_tc(const CUtensorMap& hmap, const StageOneParams& p, int BN, bool lse, int grid,
                             cudaStream_t stream);
+// p.mode 1 / 2 of the 1-CTA kernel (top-k candidates / raw logits); xform applies to mode 1.
+cudaError_t launch_fused_tc_topk(const CUtensorMap& hmap, const StageOneParams& p, int BN, int grid,
+                                 cudaStream_t stream);
 // CUDA-core stage 1: grid = ceil(V/128) aligned tiles, one slot per tile.
 cudaError_t launch_fused_simt(const StageOneParams& p, fs_dtype dtype, bool lse, cudaStream_t stream);
 
@@ -80,11 +95,20 @@ int logits_sample_blocks(int B, int V);   // V blocks of the standalone sampler 
 // then a per-row merge + top-p + Gumbel-max.
 int topk_chunks(int V);
 int topk_max_k();
+// row_offset: global batch index of row 0 (shared-stream RNG counter); the per-row arrays
+// (temperature, mask, seeds, steps, outputs) are already offset by the caller.
 cudaError_t launch_topk_sample(fs_dtype dtype, const void* logits, int64_t ld, const float* bias,
                                const float* temperature, const uint32_t* mask, int64_t mask_words, int B, int V,
                                int k, float top_p, uint64_t seed, uint64_t step, const uint64_t* seeds,
                                const uint64_t* steps, void* cand_ws, int32_t* idx_out, float* score_out,
-                               float* logZ_out, float* logprob_out, cudaStream_t stream);
+                               float* logZ_out, float* logprob_out, cudaStream_t stream, int row_offset = 0);
+// Merge stage only: cand [B][ncand] (key, id), n_b = row_count[b] (reset to 0) or ncand; slot_lb
+// [B][nslots] = each slot's m-th largest key (pruning bound) -> top-k -> top-p -> Gumbel-max.
+cudaError_t launch_topk_final(const Cand* cand, int ncand, int* row_count, int B, int k, float top_p,
+                              const float* temperature, uint64_t seed, uint64_t step, const uint64_t* seeds,
+                              const uint64_t* steps, int32_t* idx_out, float* score_out, float* logZ_out,
+                              float* logprob_out, cudaStream_t stream, int row_offset, bool pdl,
+                              const uint32_t* slot_lb, int nslots, int m);
 cudaError_t launch_combine(const fs_summary* gathered, int n, int B, int32_t* idx_out, float* score_out,
                            float* logZ_out, cudaStream_t stream);
 cudaError_t launch_merge(const fs_summary* a, const fs_summary* b, fs_summary* out, int count,

@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+python -c "import paper_2603_15854_b200" || exit 1
+DBG_NO_MMA=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:fused_tc_kernel -s 2 -c 1 -o gpurun_out/prof_topk python tools/exp_topk_one.py 32 1 50 > /dev/null 2>&1
+ncu -i gpurun_out/prof_topk.ncu-rep --page details --csv > gpurun_out/prof_topk_ties.details.csv 2>/dev/null
+ncu -i gpurun_out/prof_topk.ncu-rep --page source --csv --print-source sass > gpurun_out/prof_topk_ties.source.csv 2>/dev/null
+rm -f gpurun_out/prof_topk.ncu-rep

@@ -9,7 +9,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libflashsample.so")
+LIB_PATH = os.environ.get("FS_LIB_PATH") or os.path.join(HERE, "libflashsample.so")   # override: A/B experiments
 
 # Every symbol include/flashsample.h declares (checked by tests/test_abi.py).
 EXPORTS = [

@@ -471,9 +471,12 @@ def run_tp(args):
     from paper_2603_15854_b200 import tp
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
+    if os.environ.get("FS_TP_SAME_DEVICE"):       # test hook: all ranks on GPU 0 (gloo), for 1-GPU boxes
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    backend = os.environ.get("FS_TP_BACKEND", "nccl")
+    dist.init_process_group(backend, **({"device_id": dev} if backend == "nccl" else {}))
     name, B = args.config, args.B
     cfg = synth.CONFIGS[name]
     D, V = cfg["D"], cfg["V"]
@@ -530,6 +533,36 @@ def run_tp(args):
     torch.cuda.synchronize()
     e2e_ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
     dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    # the same step with the library's peer-memory exchange instead of the NCCL
+    # all-gather (reported beside the headline; the headline keeps the NCCL path)
+    push = {}
+    ok = torch.ones(1, device=dev)
+    try:
+        tp.PushExchange(B_max=B)
+    except Exception as e:  # pragma: no cover
+        ok.zero_()
+        push["error"] = repr(e)[:200]
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if ok.item() == 1:
+        def pstep():
+            ctr[0] += 1
+            return fs.sample_tp_push(h, W, a, V, seed=synth.SAMPLING_SEED, step=ctr[0])
+        for _ in range(max(3, args.warmup)):
+            pstep()
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0.record()
+        for _ in range(args.steps):
+            pidx = pstep()
+        e1.record()
+        torch.cuda.synchronize()
+        p_ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+        dist.all_reduce(p_ms, op=dist.ReduceOp.MAX)
+        ref = tp.sample_tp(h, W, a, V, seed=synth.SAMPLING_SEED, step=ctr[0], workspace=(local_s, gathered))
+        same = torch.tensor([float(torch.equal(ref, pidx))], device=dev)
+        dist.all_reduce(same, op=dist.ReduceOp.MIN)
+        push = {"us_per_step": round(p_ms.item() * 1e3, 2), "idx_equal_nccl_path": bool(same.item() == 1),
+                "timeouts": fs.query("comm_timeouts")}
     if rank == 0:
         pk = peaks()
         us = ms.item() * 1e3
@@ -544,6 +577,7 @@ def run_tp(args):
                 "aggregate_hbm_gbs": round(byts / (ms.item() * 1e-3) / 1e9, 1),
                 "per_rank_hbm_frac": round((2 * (b - a) * D / (ms.item() * 1e-3) / 1e9) / pk["hbm_gbs"], 4),
                 "idx_identical_across_ranks": identical,
+                "exchange_push": push,
                 "clocks": clk.summary(), "gpu_launches": 3 * args.steps,
                 "e2e": {"value": round(e2e_ms.item() * 1e3, 2), "unit": UNIT, "h2d_bytes_per_step": B * D * 2,
                         "d2h_bytes_per_step": B * 4}}

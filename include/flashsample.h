@@ -205,6 +205,38 @@ fs_status fs_combine_summaries(const fs_summary* gathered, int n, int B,
                                int32_t* idx_out, float* score_out, float* logZ_out,
                                void* stream);
 
+/* ---- Peer-memory exchange for vocabulary-sharded sampling -------------------
+ * P:830 lets the coordinator gather the shard summaries by "an all-gather ... or an equivalent
+ * reduction".  Instead of a collective call, every rank PUSHES its B x 12-byte records straight
+ * into every peer's exchange window (CUDA IPC mapping; NVLink/NVSwitch stores between GPUs) and
+ * raises a per-step flag; each rank then waits for the n flags of the step and runs the outer
+ * selection on its local copy -- one kernel after stage 2, no NCCL launch, no host round trip.
+ *   Window of a rank (device memory owned by its context): records [2 parities][world][B_max]
+ *   fs_summary, flags [2][world] uint64 (the epoch that filled the slot), acks [world] uint64
+ *   (the last epoch each reader consumed, so a writer never overwrites a parity slot that is
+ *   still unread).  Ordering: records, then fence.sys, then the flag (release); readers
+ *   acquire the flags before reading the records.
+ * fs_comm_window_create: allocate and zero this rank's window for <= B_max rows (one window per
+ *   context; replaces a previous one), return its IPC handle (64 opaque bytes) for the caller to
+ *   all-gather by any host transport (torch.distributed, gloo).  world <= 16.
+ * fs_comm_window_open: map the peers' windows from the gathered handles [world] (entry `rank`
+ *   is ignored).  Peers may be other GPUs (peer access over NVLink) or the same GPU.
+ * fs_sample_tp_push: fs_sample_shard + push + wait + fs_combine_summaries in stream order;
+ *   every rank gets the identical idx_out (score_out, logZ_out optional).  All ranks must call it
+ *   the same number of times (the step epoch is a per-context counter).  A peer that does not
+ *   arrive within ~10 s makes the wait give up: idx_out = -1 and fs_ctx_query("comm_timeouts")
+ *   counts it.
+ * fs_comm_window_destroy: unmap the peers and free the window. */
+typedef struct { unsigned char bytes[64]; } fs_ipc_handle;
+fs_status fs_comm_window_create(fs_ctx* ctx, int world, int rank, int B_max, fs_ipc_handle* handle_out);
+fs_status fs_comm_window_open(fs_ctx* ctx, const fs_ipc_handle* handles);
+fs_status fs_sample_tp_push(fs_ctx* ctx, fs_dtype dtype, const void* h, const void* W_shard,
+                            const float* bias_shard, const float* temperature, const uint32_t* mask,
+                            uint64_t seed, uint64_t step, int B, int D, int V_local,
+                            int64_t vocab_offset, int64_t V_total,
+                            int32_t* idx_out, float* score_out, float* logZ_out, void* stream);
+fs_status fs_comm_window_destroy(fs_ctx* ctx);
+
 /* fs_merge_summaries -- online binary merge of two summaries of disjoint vocabulary sets
  * (Alg. A.3, Lemma "binary merge" P:315-349, realised by max reuse):
  *   out.max_score = max, out.idx = idx of the max (ties -> smaller id),

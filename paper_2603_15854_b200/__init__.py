@@ -22,7 +22,8 @@ from ._lib import FS_BF16, FS_F32, FlashSampleError
 
 __all__ = ["sample", "sample_grouped", "sample_logits", "sample_shard", "combine_summaries", "merge_summaries",
            "random_bits", "gumbel_from_bits", "Summaries", "context", "set_option", "query",
-           "FlashSampleError", "version", "sample_from_host"]
+           "FlashSampleError", "version", "sample_from_host", "comm_window_create", "comm_window_open",
+           "comm_window_destroy", "sample_tp_push"]
 
 _ctx = {}
 
@@ -127,6 +128,42 @@ def sample(h, W, *, bias=None, temperature=None, mask=None, seed: int = 0, step:
                                        ctypes.byref(args), _stream(h)), "fs_sample_ex")
     res = (idx,) + ((score,) if return_score else ()) + ((logZ, logprob) if return_logprob else ())
     return res if len(res) > 1 else idx
+
+
+def comm_window_create(world: int, rank: int, B_max: int, device=None) -> bytes:
+    """Allocate this rank's peer-exchange window; returns its 64-byte IPC handle,
+    to be all-gathered by the caller (any host transport) and passed to comm_window_open."""
+    hd = _lib.IpcHandle()
+    _lib.check(_lib.lib().fs_comm_window_create(context(device), int(world), int(rank), int(B_max), ctypes.byref(hd)),
+               "fs_comm_window_create")
+    return bytes(hd.bytes)
+
+
+def comm_window_open(handles, device=None) -> None:
+    """Map the peers' windows from the gathered handles (list of `world` 64-byte strings)."""
+    arr = (_lib.IpcHandle * len(handles))()
+    for i, hb in enumerate(handles):
+        ctypes.memmove(arr[i].bytes, bytes(hb), 64)
+    _lib.check(_lib.lib().fs_comm_window_open(context(device), arr), "fs_comm_window_open")
+
+
+def comm_window_destroy(device=None) -> None:
+    _lib.check(_lib.lib().fs_comm_window_destroy(context(device)), "fs_comm_window_destroy")
+
+
+def sample_tp_push(h, W_shard, vocab_offset: int, V_total: int, *, bias_shard=None, temperature=None, mask=None,
+                   seed: int = 0, step: int = 0, return_all: bool = False):
+    """Vocabulary-sharded step with the peer-memory exchange (fs_sample_tp_push): shard summary,
+    push to every peer window, wait, outer selection.  idx [B] identical on all ranks."""
+    B, D, V_local = _check_inputs(h, W_shard, bias_shard, temperature, mask, V_total=V_total)
+    idx = torch.empty(B, dtype=torch.int32, device=h.device)
+    score = torch.empty(B, dtype=torch.float32, device=h.device) if return_all else None
+    logZ = torch.empty(B, dtype=torch.float32, device=h.device) if return_all else None
+    _lib.check(_lib.lib().fs_sample_tp_push(
+        context(h.device), _dtype_code(h, W_shard), _ptr(h), _ptr(W_shard), _ptr(bias_shard), _ptr(temperature),
+        _ptr(mask), seed & (2**64 - 1), step & (2**64 - 1), B, D, V_local, int(vocab_offset), int(V_total),
+        _ptr(idx), _ptr(score), _ptr(logZ), _stream(h)), "fs_sample_tp_push")
+    return (idx, score, logZ) if return_all else idx
 
 
 @dataclasses.dataclass

@@ -17,6 +17,7 @@ EXPORTS = [
     "fs_ctx_set_option", "fs_ctx_query", "fs_sample", "fs_sample_ex", "fs_sample_grouped", "fs_sample_logits",
     "fs_sample_logits_ex", "fs_sample_shard",
     "fs_combine_summaries", "fs_merge_summaries", "fs_random_bits", "fs_gumbel_from_bits",
+    "fs_comm_window_create", "fs_comm_window_open", "fs_sample_tp_push", "fs_comm_window_destroy",
 ]
 
 FS_OK, FS_ERR_INVALID, FS_ERR_UNSUPPORTED, FS_ERR_CUDA, FS_ERR_OOM = range(5)
@@ -30,6 +31,11 @@ class SampleArgs(ctypes.Structure):
                 ("score_out", ctypes.c_void_p), ("logZ_out", ctypes.c_void_p), ("logprob_out", ctypes.c_void_p),
                 ("groups_out", ctypes.c_void_p), ("top_k", ctypes.c_int), ("top_p", ctypes.c_float)]
 FS_BF16, FS_F32 = 0, 1
+
+
+class IpcHandle(ctypes.Structure):
+    """fs_ipc_handle: 64 opaque bytes (a cudaIpcMemHandle_t)."""
+    _fields_ = [("bytes", ctypes.c_ubyte * 64)]
 
 
 class FlashSampleError(RuntimeError):
@@ -71,6 +77,10 @@ def lib() -> ctypes.CDLL:
     L.fs_merge_summaries.argtypes = [vp, vp, vp, i32, vp]
     L.fs_random_bits.argtypes = [u64, u64, u32, vp, vp, vp, i64, vp]
     L.fs_gumbel_from_bits.argtypes = [vp, vp, i64, vp]
+    L.fs_comm_window_create.argtypes = [vp, i32, i32, i32, ctypes.POINTER(IpcHandle)]
+    L.fs_comm_window_open.argtypes = [vp, ctypes.POINTER(IpcHandle)]
+    L.fs_comm_window_destroy.argtypes = [vp]
+    L.fs_sample_tp_push.argtypes = [vp, i32, vp, vp, vp, vp, vp, u64, u64, i32, i32, i32, i64, i64, vp, vp, vp, vp]
     for name in EXPORTS:
         if name not in ("fs_version", "fs_status_str", "fs_last_error", "fs_ctx_destroy"):
             getattr(L, name).restype = i32

@@ -53,6 +53,14 @@ struct fs_ctx {
   int pair_min_bn = 32;            // auto: use the pair kernel from this MMA N upwards (measured)
   int topk_mode = 0;               // fused top-k: 0 auto, 1 candidate lists in the epilogue, 2 via raw logits
   int* topk_rowcnt = nullptr;      // [256] per-row candidate counters of the list route (kept at 0 between calls)
+  // f2 peer-memory exchange (fs_comm_window_*)
+  char* comm_win = nullptr;        // this rank's window (cudaMalloc, exported by IPC)
+  size_t comm_off_flags = 0, comm_off_acks = 0, comm_off_status = 0;
+  int comm_world = 0, comm_rank = 0, comm_bmax = 0;
+  char* comm_peer[fs::kMaxWorld] = {};
+  bool comm_open = false;
+  fs_summary* comm_local = nullptr;   // [B_max] this rank's shard summaries
+  uint64_t comm_epoch = 0;
   // tensor-map cache: encoding costs host microseconds per map; W maps are reused across calls
   struct MapKey { const void* base; int64_t inner, rows; int box, promo; };
   struct MapEnt { MapKey k; CUtensorMap m; };
@@ -500,6 +508,7 @@ void fs_ctx_destroy(fs_ctx* ctx) {
   }
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->topk_rowcnt) cudaFree(ctx->topk_rowcnt);
+  fs_comm_window_destroy(ctx);
   delete ctx;
 }
 
@@ -549,6 +558,15 @@ fs_status fs_ctx_query(fs_ctx* ctx, const char* name, double* out) {
     }
     ctx->ev_used = 0;
     *out = total;
+    return FS_OK;
+  }
+  if (!strcmp(name, "comm_timeouts")) {
+    unsigned t = 0;
+    if (ctx->comm_win) {
+      cudaError_t e = cudaMemcpy(&t, ctx->comm_win + ctx->comm_off_status, sizeof(t), cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) return cuda_fail(e, "comm status read");
+    }
+    *out = (double)t;
     return FS_OK;
   }
   if (!strcmp(name, "num_sms")) {
@@ -685,6 +703,92 @@ fs_status fs_sample_ex(fs_ctx* ctx, fs_dtype dtype, const void* h, const void* W
              B, D, V, 0, gs, lse, args->idx_out, args->score_out, args->logZ_out, args->groups_out, n_groups,
              args->logprob_out, args->seeds, args->steps};
   return run_path(ctx, a, static_cast<cudaStream_t>(stream));
+}
+
+fs_status fs_comm_window_create(fs_ctx* ctx, int world, int rank, int B_max, fs_ipc_handle* handle_out) {
+  if (!ctx || !handle_out) return fail(FS_ERR_INVALID, "ctx and handle_out are required");
+  if (world < 1 || world > fs::kMaxWorld || rank < 0 || rank >= world || B_max < 1)
+    return fail(FS_ERR_INVALID, "need 1 <= world <= 16, 0 <= rank < world, B_max >= 1");
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  fs_comm_window_destroy(ctx);
+  const size_t rec = (size_t)2 * world * B_max * sizeof(fs_summary);
+  ctx->comm_off_flags = (rec + 127) & ~size_t(127);
+  ctx->comm_off_acks = ctx->comm_off_flags + (((size_t)2 * world * 8 + 127) & ~size_t(127));
+  ctx->comm_off_status = ctx->comm_off_acks + (((size_t)world * 8 + 127) & ~size_t(127));
+  const size_t bytes = ctx->comm_off_status + 128;
+  if ((e = cudaMalloc(&ctx->comm_win, bytes)) != cudaSuccess) return fail(FS_ERR_OOM, "window cudaMalloc failed");
+  if ((e = cudaMemset(ctx->comm_win, 0, bytes)) != cudaSuccess) return cuda_fail(e, "window memset");
+  if ((e = cudaMalloc(&ctx->comm_local, (size_t)B_max * sizeof(fs_summary))) != cudaSuccess)
+    return fail(FS_ERR_OOM, "summary cudaMalloc failed");
+  cudaIpcMemHandle_t h;
+  if ((e = cudaIpcGetMemHandle(&h, ctx->comm_win)) != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+  static_assert(sizeof(h) <= sizeof(fs_ipc_handle), "IPC handle size");
+  std::memset(handle_out, 0, sizeof(*handle_out));
+  std::memcpy(handle_out->bytes, &h, sizeof(h));
+  ctx->comm_world = world;
+  ctx->comm_rank = rank;
+  ctx->comm_bmax = B_max;
+  ctx->comm_epoch = 0;
+  return FS_OK;
+}
+
+fs_status fs_comm_window_open(fs_ctx* ctx, const fs_ipc_handle* handles) {
+  if (!ctx || !handles) return fail(FS_ERR_INVALID, "ctx and handles are required");
+  if (!ctx->comm_win) return fail(FS_ERR_INVALID, "fs_comm_window_create first");
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  for (int p = 0; p < ctx->comm_world; ++p) {
+    if (p == ctx->comm_rank) { ctx->comm_peer[p] = ctx->comm_win; continue; }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handles[p].bytes, sizeof(h));
+    void* ptr = nullptr;
+    if ((e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess)) != cudaSuccess)
+      return cuda_fail(e, "cudaIpcOpenMemHandle");
+    ctx->comm_peer[p] = static_cast<char*>(ptr);
+  }
+  ctx->comm_open = true;
+  return FS_OK;
+}
+
+fs_status fs_comm_window_destroy(fs_ctx* ctx) {
+  if (!ctx) return fail(FS_ERR_INVALID, "ctx is NULL");
+  cudaSetDevice(ctx->device);
+  if (ctx->comm_open)
+    for (int p = 0; p < ctx->comm_world; ++p)
+      if (p != ctx->comm_rank && ctx->comm_peer[p]) cudaIpcCloseMemHandle(ctx->comm_peer[p]);
+  for (auto& q : ctx->comm_peer) q = nullptr;
+  ctx->comm_open = false;
+  if (ctx->comm_win) cudaFree(ctx->comm_win);
+  if (ctx->comm_local) cudaFree(ctx->comm_local);
+  ctx->comm_win = nullptr;
+  ctx->comm_local = nullptr;
+  ctx->comm_world = 0;
+  return FS_OK;
+}
+
+fs_status fs_sample_tp_push(fs_ctx* ctx, fs_dtype dtype, const void* h, const void* W_shard, const float* bias_shard,
+                            const float* temperature, const uint32_t* mask, uint64_t seed, uint64_t step, int B, int D,
+                            int V_local, int64_t vocab_offset, int64_t V_total, int32_t* idx_out, float* score_out,
+                            float* logZ_out, void* stream) {
+  if (!ctx || !ctx->comm_open) return fail(FS_ERR_INVALID, "open the exchange window first (fs_comm_window_open)");
+  if (!idx_out) return fail(FS_ERR_INVALID, "idx_out is required");
+  if (B > ctx->comm_bmax) return fail(FS_ERR_INVALID, "B exceeds the window's B_max");
+  fs_status s = fs_sample_shard(ctx, dtype, h, W_shard, bias_shard, temperature, mask, seed, step, B, D, V_local,
+                                vocab_offset, V_total, ctx->comm_local, stream);
+  if (s != FS_OK) return s;
+  fs::PeerTab peers{};
+  for (int p = 0; p < ctx->comm_world; ++p) {
+    peers.rec[p] = reinterpret_cast<fs_summary*>(ctx->comm_peer[p]);
+    peers.flags[p] = reinterpret_cast<uint64_t*>(ctx->comm_peer[p] + ctx->comm_off_flags);
+    peers.acks[p] = reinterpret_cast<uint64_t*>(ctx->comm_peer[p] + ctx->comm_off_acks);
+  }
+  const uint64_t epoch = ++ctx->comm_epoch;
+  cudaError_t e = fs::launch_exchange_combine(ctx->comm_local, peers, ctx->comm_world, ctx->comm_rank, B,
+                                              ctx->comm_bmax, epoch, idx_out, score_out, logZ_out,
+                                              reinterpret_cast<unsigned*>(ctx->comm_win + ctx->comm_off_status),
+                                              static_cast<cudaStream_t>(stream), ctx->pdl != 0);
+  return e == cudaSuccess ? FS_OK : cuda_fail(e, "exchange kernel launch");
 }
 
 fs_status fs_combine_summaries(const fs_summary* gathered, int n, int B, int32_t* idx_out, float* score_out,

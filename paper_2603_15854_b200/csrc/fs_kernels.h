@@ -109,6 +109,17 @@ cudaError_t launch_topk_final(const Cand* cand, int ncand, int* row_count, int B
                               const uint64_t* steps, int32_t* idx_out, float* score_out, float* logZ_out,
                               float* logprob_out, cudaStream_t stream, int row_offset, bool pdl,
                               const uint32_t* slot_lb, int nslots, int m);
+// Peer windows of the f2 exchange (fs_reduce.cu): per rank, records [2][world][B_max], flags
+// [2][world] and acks [world] (see include/flashsample.h fs_comm_window_create).
+constexpr int kMaxWorld = 16;
+struct PeerTab {
+  fs_summary* rec[kMaxWorld];
+  uint64_t* flags[kMaxWorld];
+  uint64_t* acks[kMaxWorld];
+};
+cudaError_t launch_exchange_combine(const fs_summary* local, const PeerTab& peers, int world, int rank, int B,
+                                    int B_max, uint64_t epoch, int32_t* idx_out, float* score_out, float* logZ_out,
+                                    unsigned* timeouts, cudaStream_t stream, bool pdl);
 cudaError_t launch_combine(const fs_summary* gathered, int n, int B, int32_t* idx_out, float* score_out,
                            float* logZ_out, cudaStream_t stream);
 cudaError_t launch_merge(const fs_summary* a, const fs_summary* b, fs_summary* out, int count,

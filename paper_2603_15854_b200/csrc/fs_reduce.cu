@@ -215,6 +215,96 @@ cudaError_t launch_reduce(const State* part, const int* part_group, const SlotLa
                             score_out, logZ_out, groups_out, logprob_out);
 }
 
+// ---------------------------------------------------------------------------------------------
+// Peer-memory exchange ("all-gather ... or an equivalent reduction").
+// One CTA: (1) wait until every reader consumed the previous use of this parity slot, (2) store
+// this rank's B records into slot [parity][rank] of every peer window, fence.sys, release the
+// flags, (3) acquire the n flags of this epoch in the local window, (4) outer selection over the
+// n local records per row, (5) ack the epoch into every peer window.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Spin until pred(ld_acquire(p)) or ~10 s; false on timeout.
+template <typename Pred>
+__device__ __forceinline__ bool wait_flag(const uint64_t* p, Pred pred) {
+  const uint64_t t0 = globaltimer_ns();
+  uint32_t ns = 32;
+  while (!pred(ld_acquire_sys(p))) {
+    if (globaltimer_ns() - t0 > 10000000000ull) return false;
+    __nanosleep(ns);
+    ns = ns < 1024 ? ns * 2 : ns;
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(256)
+exchange_combine_kernel(const fs_summary* __restrict__ local, PeerTab peers, int world, int rank, int B, int B_max,
+                        uint64_t epoch, int32_t* idx_out, float* score_out, float* logZ_out, unsigned* timeouts) {
+  __shared__ int ok;
+  sm100::pdl_wait();                                   // the shard summaries are complete
+  const int par = (int)(epoch & 1);
+  if (threadIdx.x == 0) ok = 1;
+  __syncthreads();
+  const uint64_t prev = epoch >= 2 ? epoch - 2 : 0;
+  if (threadIdx.x < world)                            // reader `tid` finished the last use of slot `par`
+    if (!wait_flag(peers.acks[rank] + threadIdx.x, [&](uint64_t v) { return v >= prev; })) ok = 0;
+  __syncthreads();
+  for (int p = 0; p < world; ++p) {
+    fs_summary* dst = peers.rec[p] + ((size_t)par * world + rank) * B_max;
+    for (int b = threadIdx.x; b < B; b += blockDim.x) dst[b] = local[b];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int p = 0; p < world; ++p) st_release_sys(peers.flags[p] + par * world + rank, epoch);
+  }
+  if (threadIdx.x < world)
+    if (!wait_flag(peers.flags[rank] + par * world + threadIdx.x, [&](uint64_t v) { return v == epoch; })) ok = 0;
+  __syncthreads();
+  const fs_summary* rec = peers.rec[rank] + (size_t)par * world * B_max;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    State acc = state_empty();
+    for (int k = 0; k < world; ++k) acc = state_merge(acc, from_summary(rec[(size_t)k * B_max + b]));
+    const fs_summary f = to_summary(acc);
+    idx_out[b] = ok ? f.idx : -1;
+    if (score_out) score_out[b] = f.max_score;
+    if (logZ_out) logZ_out[b] = f.log_mass;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (!ok) atomicAdd(timeouts, 1u);
+    for (int p = 0; p < world; ++p) st_release_sys(peers.acks[p] + rank, epoch);
+  }
+}
+
+cudaError_t launch_exchange_combine(const fs_summary* local, const PeerTab& peers, int world, int rank, int B,
+                                    int B_max, uint64_t epoch, int32_t* idx_out, float* score_out, float* logZ_out,
+                                    unsigned* timeouts, cudaStream_t stream, bool pdl) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.stream = stream;
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(256);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, exchange_combine_kernel, local, peers, world, rank, B, B_max, epoch, idx_out,
+                            score_out, logZ_out, timeouts);
+}
+
 cudaError_t launch_combine(const fs_summary* gathered, int n, int B, int32_t* idx_out, float* score_out,
                            float* logZ_out, cudaStream_t stream) {
   combine_kernel<<<(B + 127) / 128, 128, 0, stream>>>(gathered, n, B, idx_out, score_out, logZ_out);

@@ -9,13 +9,17 @@ keyed by global vocabulary ids and no logit's fp32 accumulation depends on the s
 result equals single-GPU fs_sample bit for bit.
 
 The exchange is torch.distributed plumbing; all arithmetic runs in the library kernels.
+transport="push" replaces the collective by the library's peer-memory
+exchange: every rank stores its records into every peer's window (CUDA IPC; NVLink stores
+between GPUs) and one kernel after stage 2 waits for the n records and combines them.  The
+torch.distributed group is then used once, to all-gather the 64-byte window handles.
 """
 from __future__ import annotations
 
 import torch
 import torch.distributed as dist
 
-from . import Summaries, combine_summaries, sample_shard
+from . import Summaries, combine_summaries, comm_window_create, comm_window_open, sample_shard, sample_tp_push
 
 
 def shard_bounds(V: int, world: int, rank: int) -> tuple[int, int]:
@@ -44,3 +48,21 @@ def sample_tp(h, W_shard, vocab_offset: int, V_total: int, *, group=None, bias_s
                          mask=mask, seed=seed, step=step, out=local)
     gathered = gather_summaries(local.raw, group=group, out=gathered)
     return combine_summaries(gathered, return_all=return_all)
+
+
+class PushExchange:
+    """Peer-memory exchange windows of a process group (one per rank, up to B_max rows).
+    Creating it is collective: every rank all-gathers its window handle over `group`."""
+
+    def __init__(self, B_max: int, group=None, device=None):
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        handle = comm_window_create(world, rank, B_max, device=device)
+        handles = [None] * world
+        dist.all_gather_object(handles, handle, group=group)
+        comm_window_open(handles, device=device)
+        self.world, self.rank, self.B_max = world, rank, B_max
+
+
+def sample_tp_push_step(h, W_shard, vocab_offset: int, V_total: int, **kw):
+    """One sharded step over an opened PushExchange (same arguments as sample_tp)."""
+    return sample_tp_push(h, W_shard, vocab_offset, V_total, **kw)

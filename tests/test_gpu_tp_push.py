@@ -1,0 +1,78 @@
+"""GPU test of the peer-memory TP exchange ("an equivalent reduction";
+include/flashsample.h fs_comm_window_* / fs_sample_tp_push).
+
+Only one GPU is available, so the ranks are separate processes on the SAME device: each maps the
+others' exchange windows through CUDA IPC and the push/flag/ack protocol runs exactly as between
+GPUs (the stores just do not cross NVLink).  Every rank must return the single-GPU fs_sample
+result bit for bit (shards keyed by global ids, no split-K), over several consecutive steps so
+both parity slots and the reader acknowledgements are exercised."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, cfg, B, V, D, steps, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        import synth
+        import paper_2603_15854_b200 as fs
+        from paper_2603_15854_b200 import tp
+        wl = synth.make_workload(cfg, B, V=V, D=D, seed_offset=world)
+        dev = torch.device("cuda", 0)
+        h, W = wl.h.to(dev), wl.W.to(dev)
+        bias = None if wl.bias is None else wl.bias.to(dev)
+        tau = None if wl.temperature is None else wl.temperature.to(dev)
+        mask = None if wl.mask is None else wl.mask.to(dev)
+        lo, hi = tp.shard_bounds(V, world, rank)
+        tp.PushExchange(B_max=B)
+        out = []
+        for s in range(steps):
+            idx, score, logZ = tp.sample_tp_push_step(
+                h, W[lo:hi].contiguous(), lo, V, bias_shard=None if bias is None else bias[lo:hi].contiguous(),
+                temperature=tau, mask=mask, seed=wl.seed, step=s, return_all=True)
+            ref_idx, ref_score = fs.sample(h, W, bias=bias, temperature=tau, mask=mask, seed=wl.seed, step=s,
+                                           return_score=True)
+            out.append((torch.equal(idx, ref_idx), torch.equal(score.view(torch.int32), ref_score.view(torch.int32)),
+                        bool(torch.isfinite(logZ).all())))
+        timeouts = fs.query("comm_timeouts")
+        dist.barrier()                       # peers stay mapped until everyone is done
+        fs.comm_window_destroy()
+        q.put((rank, out, timeouts, None))
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put((rank, None, None, repr(e)))
+
+
+@pytest.mark.parametrize("world,cfg,B,V,D", [(2, "llama3_8b", 8, 20011, 256), (3, "qwen25_7b", 33, 9001, 128),
+                                             (4, "llama3_8b", 1, 4096, 64)])
+def test_push_exchange_matches_single_gpu(world, cfg, B, V, D):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, B, V, D, 5, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, out, timeouts, err in res:
+        assert err is None, (rank, err)
+        assert timeouts == 0
+        assert all(a and b and c for a, b, c in out), (rank, out)

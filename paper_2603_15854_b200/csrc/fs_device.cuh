@@ -33,10 +33,35 @@ __device__ __forceinline__ U4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c
   return U4{c0, c1, c2, c3};
 }
 
+__device__ __forceinline__ uint32_t sel4(uint32_t x, uint32_t y, uint32_t z, uint32_t w, int i) {
+  return i == 0 ? x : i == 1 ? y : i == 2 ? z : w;
+}
+
+// Per-request draws (reading R18: key = seed_b, counter = (v >> 2, 2^31, step_b), word v & 3) of
+// 4 batch columns for a warp whose lanes 4g..4g+3 hold vocabulary ids 4m..4m+3 (one counter per
+// lane quartet).  Instead of 4 Philox calls per lane, lane a = lane & 3 evaluates the call of
+// column a (its key / counter words k0..c3 are passed in) and 4 shuffle rounds hand every lane
+// word (v & 3) of each column: round r, lane s sends word (a_s - r) & 3 and lane d reads lane
+// (a_d + r) & 3 of its quartet, i.e. the word of column (a_d + r) & 3.  Warp-converged callers only.
+__device__ __forceinline__ void prq_bits4(uint32_t vq, uint32_t k0, uint32_t k1, uint32_t c2, uint32_t c3, int lane,
+                                          uint32_t (&rr)[4]);
+
 // Counter words 2 and 3 for (step, tag).
 __device__ __forceinline__ uint32_t ctr_step_lo(uint64_t step) { return (uint32_t)step; }
 __device__ __forceinline__ uint32_t ctr_step_hi(uint64_t step, uint32_t tag) {
   return ((uint32_t)(step >> 32) & 0x00FFFFFFu) | (tag << 24);
+}
+
+__device__ __forceinline__ void prq_bits4(uint32_t vq, uint32_t k0, uint32_t k1, uint32_t c2, uint32_t c3, int lane,
+                                          uint32_t (&rr)[4]) {
+  const U4 o = philox4x32_10(vq, 0x80000000u, c2, c3, k0, k1);
+  const int a = lane & 3;
+  uint32_t got[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+    got[r] = __shfl_sync(0xFFFFFFFFu, sel4(o.x, o.y, o.z, o.w, (a - r) & 3), (lane & ~3) | ((a + r) & 3));
+#pragma unroll
+  for (int c = 0; c < 4; ++c) rr[c] = sel4(got[0], got[1], got[2], got[3], (c - a) & 3);
 }
 
 // ---------------------------------------------------------------------------------------

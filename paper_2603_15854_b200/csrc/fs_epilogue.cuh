@@ -104,8 +104,13 @@ __device__ __forceinline__ void epi_columns(const float* acc, int col0, const Ro
     if (b0 >= ea.B) break;                                   // warp-uniform
     uint32_t rr[4];
     if (PRQ) {
+      if (ra.warp_v0 & 3) {
 #pragma unroll
-      for (int jj = 0; jj < 4; ++jj) rr[jj] = per_request_bits(ea.tab, ra.v_lo, b0 + jj);
+        for (int jj = 0; jj < 4; ++jj) rr[jj] = per_request_bits(ea.tab, ra.v_lo, b0 + jj);
+      } else {
+        const int bq = b0 + (lane & 3);
+        prq_bits4(ra.v_lo >> 2, ea.tab->k0[bq], ea.tab->k1[bq], ea.tab->c2[bq], ea.tab->c3[bq], lane, rr);
+      }
     } else {
       const U4 r4 = philox4x32_10(ra.v_lo, (uint32_t)(ea.row_offset + b0) >> 2, ea.c2, ea.c3, ea.k0, ea.k1);
       rr[0] = r4.x; rr[1] = r4.y; rr[2] = r4.z; rr[3] = r4.w;
@@ -166,11 +171,12 @@ __device__ __forceinline__ void flush_states(State (&st)[NCHUNK], State* scratch
 // Running states: st[c] holds this lane's state for column 32c + lane; chunk c is processed at
 // st[0] and the array is rotated, so the loops stay rolled (small code, no local memory).
 // ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ void rotate_states(State (&st)[8]) {
+template <int NST>
+__device__ __forceinline__ void rotate_states(State (&st)[NST]) {
   const State t = st[0];
 #pragma unroll
-  for (int i = 0; i < 7; ++i) st[i] = st[i + 1];
-  st[7] = t;
+  for (int i = 0; i < NST - 1; ++i) st[i] = st[i + 1];
+  st[NST - 1] = t;
 }
 
 // Release of the accumulator buffer after the tile's last TMEM read: every thread arrives on the
@@ -189,14 +195,22 @@ __device__ __forceinline__ void release_tmem(uint64_t* tempty, uint32_t tempty_c
 // NG groups of 8 columns per iteration (NG = 2 doubles the independent work in flight: 4 Philox
 // chains, 16 Gumbel evaluations, 16 warp reductions -- the epilogue is latency-bound at one warp
 // pair per SM sub-partition).  Columns >= B are computed on padding and never stored.
-template <bool LSE, bool XFORM, int NG, bool PRQ = false>
-__device__ __forceinline__ void epi_tile_tc(uint32_t taddr, const RowArgs& ra, const EpiArgs& ea, State (&st)[8],
-                                            int lane, uint64_t* tempty, uint32_t tempty_cluster = 0) {
+// The warp processes the 32-column chunks c = chunk0, chunk0 + cstep, ... (cstep 2: two warps
+// per TMEM lane quadrant split a tile's columns); st[i] holds its i-th chunk.
+template <bool LSE, bool XFORM, int NG, bool PRQ = false, int NST = 8>
+__device__ __forceinline__ void epi_tile_tc(uint32_t taddr, const RowArgs& ra, const EpiArgs& ea, State (&st)[NST],
+                                            int lane, uint64_t* tempty, uint32_t tempty_cluster = 0, int chunk0 = 0,
+                                            int cstep = 1) {
   constexpr int NC = 8 * NG;
   const int B = ea.B;
   const int nch = (B + 31) >> 5;
+  const int nmine = nch > chunk0 ? (nch - chunk0 + cstep - 1) / cstep : 0;
+  if (nmine == 0) {                                   // nothing in this tile for this warp
+    release_tmem(tempty, tempty_cluster, lane);
+    return;
+  }
 #pragma unroll 1
-  for (int c = 0; c < nch; ++c) {
+  for (int c = chunk0; c < nch; c += cstep) {
     State own = st[0];
 #pragma unroll 1
     for (int g = 0; g < 4; g += NG) {
@@ -208,7 +222,7 @@ __device__ __forceinline__ void epi_tile_tc(uint32_t taddr, const RowArgs& ra, c
         sm100::tmem_ld_32x32b_x8(taddr + (uint32_t)(col0 + 8 * i), *reinterpret_cast<uint32_t(*)[8]>(&r[8 * i]));
       if (ea.dbg_skip) {
         sm100::tmem_wait_ld();
-        if (col0 + NC >= B) release_tmem(tempty, tempty_cluster, lane);
+        if (col0 + NC >= B || (c + cstep >= nch && g + NG >= 4)) release_tmem(tempty, tempty_cluster, lane);
         if (r[0] == 0x7FFFFFFFu && r[NC - 1] == 0x7FFFFFFFu) own.key = 1u;   // keep the loads live
         continue;
       }
@@ -224,9 +238,18 @@ __device__ __forceinline__ void epi_tile_tc(uint32_t taddr, const RowArgs& ra, c
       }
       // randomness: independent of the accumulator, overlaps the TMEM load
       float gm[NC];
-      if (PRQ) {                                 // per-request streams: one Philox per element
+      if (PRQ && (ra.warp_v0 & 3)) {             // unaligned shard offset: one Philox per element
 #pragma unroll
         for (int jj = 0; jj < NC; ++jj) gm[jj] = gumbel32(per_request_bits(ea.tab, ra.v_lo, col0 + jj));
+      } else if (PRQ) {                          // lane quartets share v >> 2: one Philox per 4 elements
+#pragma unroll
+        for (int qq = 0; qq < NC / 4; ++qq) {
+          const int bq = col0 + 4 * qq + (lane & 3);
+          uint32_t rr[4];
+          prq_bits4(ra.v_lo >> 2, ea.tab->k0[bq], ea.tab->k1[bq], ea.tab->c2[bq], ea.tab->c3[bq], lane, rr);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) gm[4 * qq + c] = gumbel32(rr[c]);
+        }
       } else {
         const uint32_t qd = (uint32_t)(ea.row_offset + col0) >> 2;
 #pragma unroll
@@ -239,7 +262,8 @@ __device__ __forceinline__ void epi_tile_tc(uint32_t taddr, const RowArgs& ra, c
         }
       }
       sm100::tmem_wait_ld();
-      if (col0 + NC >= B) release_tmem(tempty, tempty_cluster, lane);   // last TMEM read of the tile
+      if (col0 + NC >= B || (c + cstep >= nch && g + NG >= 4))        // this warp's last TMEM read
+        release_tmem(tempty, tempty_cluster, lane);
       uint32_t key[NC];
       float lt[NC];
 #pragma unroll
@@ -322,19 +346,21 @@ __device__ __forceinline__ void epi_tile_tc(uint32_t taddr, const RowArgs& ra, c
       }
     }
     st[0] = own;
-    if (nch > 1) rotate_states(st);
+    if (nmine > 1) rotate_states(st);
   }
-  if (nch > 1)
+  if (nmine > 1)
 #pragma unroll 1
-    for (int i = nch; i < 8; ++i) rotate_states(st);       // restore chunk order
+    for (int i = nmine; i < NST; ++i) rotate_states(st);    // restore chunk order
 }
 
 // Write this warp's states (one candidate per column for its 32 rows of every tile it saw in
 // the segment) to its own candidate slot; stage 2 merges slots (no intra-CTA barrier needed).
-__device__ __forceinline__ void flush_warp(State (&st)[8], int lane, int B, State* part_row) {
+template <int NST>
+__device__ __forceinline__ void flush_warp(State (&st)[NST], int lane, int B, State* part_row, int chunk0 = 0,
+                                           int cstep = 1) {
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const int b = c * 32 + lane;
+  for (int c = 0; c < NST; ++c) {
+    const int b = (chunk0 + c * cstep) * 32 + lane;
     if (b < B) part_row[b] = st[c];
     st[c] = state_empty();
   }

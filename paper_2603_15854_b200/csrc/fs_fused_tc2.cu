@@ -13,7 +13,10 @@
 //              the leader's producer arms it with the pair's byte count.
 //   empty[s]   one per CTA, arrived by the leader's multicast tcgen05.commit.
 //   tfull[b]   one per CTA, arrived by the multicast commit after a tile's last MMA.
-//   tempty[b]  leader's barrier, 8 arrivals: lane 0 of the 4 epilogue warps of set b in each CTA.
+//   tempty[b]  leader's barrier, 16 arrivals: lane 0 of the 8 epilogue warps of set b in each CTA.
+// Epilogue: 16 warps per CTA; set s = buffer s, and the two warps of a TMEM lane quadrant in a
+// set split the tile's 32-column chunks (even / odd) -- twice the warps of the 1-CTA kernel, for
+// latency hiding at the large batches this kernel serves.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -23,7 +26,8 @@
 namespace fs {
 
 namespace {
-constexpr int kEpiWarps = 8;
+constexpr int kEpiWarps = 16;                  // 2 sets (TMEM buffers) x 2 column halves x 4 lane quadrants
+constexpr int kSlotWarps = 8;                  // candidate slots per (segment, CTA): one per (set, quadrant)
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kBlockK = 64;
 constexpr int kWBytes = 128 * kBlockK * 2;                  // this CTA's 128 W rows per K slice
@@ -68,7 +72,7 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
     }
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&tfull[i], 1);
-      sm100::mbar_init(&tempty[i], 8);
+      sm100::mbar_init(&tempty[i], 16);
     }
     sm100::fence_barrier_init();
   }
@@ -155,8 +159,10 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
   } else {
     // -------------------------------- epilogue (both CTAs) ------------------------------
     const int e = warp - 2;
-    const int set = e >> 2;
+    const int set = e >> 3;
+    const int half = (e >> 2) & 1;                  // chunks half, half + 2, ...
     const int q = warp & 3;
+    const int sw = set * 4 + (e & 3);               // candidate slot of (set, quadrant)
     EpiArgs ea;
     ea.invtau = tab->invtau;
     ea.tab = tab;
@@ -170,10 +176,10 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
     ea.c3 = ctr_step_hi(p.step, 0u);
     ea.dbg_skip = p.dbg_no_epi;
     const uint32_t tempty_leader = sm100::mapa(sm100::smem_u32(&tempty[set]), 0);
-    State st[8];
+    State st[4];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) st[c] = state_empty();
-    const int slot0 = pair * p.max_seg;   // slot = ((pair*max_seg + seg)*2 + rank)*8 + warp
+    for (int c = 0; c < 4; ++c) st[c] = state_empty();
+    const int slot0 = pair * p.max_seg;   // slot = ((pair*max_seg + seg)*2 + rank)*8 + sw
     int tile_i = 0, seg = 0;
     for (int a = r0; a < r1; ++seg) {
       const int b = seg_end2(a, r1, gs);
@@ -191,12 +197,11 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
         ra.warp_v0 = (int32_t)(p.vocab_offset + base + 32 * q);
         ra.bias = (XFORM && ra.valid && p.bias) ? p.bias[row] : 0.0f;
         const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(set * BN);
-        if (p.B <= 8) epi_tile_tc<LSE, XFORM, 1, PRQ>(taddr, ra, ea, st, lane, &tempty[set], tempty_leader);
-        else epi_tile_tc<LSE, XFORM, 2, PRQ>(taddr, ra, ea, st, lane, &tempty[set], tempty_leader);
+        epi_tile_tc<LSE, XFORM, 1, PRQ>(taddr, ra, ea, st, lane, &tempty[set], tempty_leader, half, 2);
       }
       if (gs < p.V) {
-        const int slot = ((slot0 + seg) * 2 + (int)rank) * kEpiWarps + e;
-        flush_warp(st, lane, p.B, p.part + (size_t)slot * p.B);
+        const int slot = ((slot0 + seg) * 2 + (int)rank) * kSlotWarps + sw;
+        flush_warp(st, lane, p.B, p.part + (size_t)slot * p.B, half, 2);
         if (lane == 0) p.part_group[slot] = a / gs;
       }
       a = b;
@@ -206,25 +211,25 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
       // non-decreasing over ALL slots (stage 2 finds a group's slots by binary search)
       const int last_group = (r1 > r0 ? r1 - 1 : r0) / gs;
       for (int s = seg; s < p.max_seg; ++s) {
-        const int slot = ((slot0 + s) * 2 + (int)rank) * kEpiWarps + e;
-        flush_warp(st, lane, p.B, p.part + (size_t)slot * p.B);
+        const int slot = ((slot0 + s) * 2 + (int)rank) * kSlotWarps + sw;
+        flush_warp(st, lane, p.B, p.part + (size_t)slot * p.B, half, 2);
         if (lane == 0) p.part_group[slot] = last_group;
       }
     } else {
       // all tiles drained -> this CTA's ring is free (the leader's MMAs no longer read it)
       sm100::named_bar_sync(1, 32 * kEpiWarps);
-      State* scratch = reinterpret_cast<State*>(w_ring);
+      State* scratch = reinterpret_cast<State*>(w_ring);        // [8 (set, quadrant)][BN]
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const int bb = c * 32 + lane;
-        if (bb < BN) scratch[e * BN + bb] = st[c];
+      for (int c = 0; c < 4; ++c) {
+        const int bb = (half + 2 * c) * 32 + lane;
+        if (bb < BN) scratch[sw * BN + bb] = st[c];
       }
       sm100::named_bar_sync(1, 32 * kEpiWarps);
       const int et = threadIdx.x - 64;
       for (int bb = et; bb < p.B; bb += 32 * kEpiWarps) {
         State m = scratch[bb];
 #pragma unroll
-        for (int w = 1; w < kEpiWarps; ++w) m = state_merge(m, scratch[w * BN + bb]);
+        for (int w = 1; w < kSlotWarps; ++w) m = state_merge(m, scratch[w * BN + bb]);
         p.part[(size_t)blockIdx.x * p.B + bb] = m;
       }
       if (et == 0) p.part_group[blockIdx.x] = (r0 < r1) ? 0 : -1;

@@ -67,7 +67,10 @@ logits_sample_kernel(const T* __restrict__ logits, int64_t ld, const float* __re
 #pragma unroll
   for (int j = 0; j < 4; ++j) st[j] = state_empty();
   // 4 columns per iteration (v, v+256, v+512, v+768): all 16 loads issued before the RNG work
-  for (int v0 = v_begin + (int)threadIdx.x; v0 < v_end; v0 += 1024) {
+  // warp-uniform trip count (the per-request exchange shuffles across the warp); lanes past
+  // v_end load -inf and are masked below
+  for (int vw = v_begin + (int)(threadIdx.x & ~31u); vw < v_end; vw += 1024) {
+    const int v0 = vw + (int)(threadIdx.x & 31u);
     float lv[4][4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -79,16 +82,17 @@ logits_sample_kernel(const T* __restrict__ logits, int64_t ld, const float* __re
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int v = v0 + 256 * u;
-      if (v >= v_end) break;
       uint32_t rr[4];
       if (PRQ) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const U4 o = philox4x32_10((uint32_t)v >> 2, 0x80000000u, pc2[j], pc3[j], pk0[j], pk1[j]);
-          const uint32_t sel = (uint32_t)v & 3u;
-          rr[j] = sel == 0 ? o.x : sel == 1 ? o.y : sel == 2 ? o.z : o.w;
-        }
-      } else {
+        // lane quartets hold v = 4m..4m+3 (v_begin % 4 == 0): one Philox per 4 elements, computed
+        // before the range test so that the whole warp takes part in the exchange
+        const int a = threadIdx.x & 3;
+        prq_bits4((uint32_t)v >> 2, sel4(pk0[0], pk0[1], pk0[2], pk0[3], a), sel4(pk1[0], pk1[1], pk1[2], pk1[3], a),
+                  sel4(pc2[0], pc2[1], pc2[2], pc2[3], a), sel4(pc3[0], pc3[1], pc3[2], pc3[3], a),
+                  (int)(threadIdx.x & 31), rr);
+      }
+      if (v >= v_end) continue;
+      if (!PRQ) {
         const U4 r4 = philox4x32_10((uint32_t)v, (uint32_t)b0 >> 2, c2, c3, k0, k1);
         rr[0] = r4.x; rr[1] = r4.y; rr[2] = r4.z; rr[3] = r4.w;
       }

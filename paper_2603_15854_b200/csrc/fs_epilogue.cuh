@@ -230,6 +230,7 @@ __device__ __forceinline__ void epi_tile_tc(uint32_t taddr, const RowArgs& ra, c
       // (col0+j, w0+1), w0 = first word of the warp's 32 rows (rows may straddle two words)
       uint32_t mw = 0xFFFFFFFFu;
       const int wshift = ra.warp_v0 & 31;
+      const int msrc = ((lane + wshift) >> 5) << 4, mbit = (lane + wshift) & 31;
       if (XFORM && ea.mask != nullptr) {
         const int jb = col0 + (lane & 15);
         const int64_t w = (int64_t)(ra.warp_v0 >> 5) + (lane >> 4);
@@ -274,9 +275,9 @@ __device__ __forceinline__ void epi_tile_tc(uint32_t taddr, const RowArgs& ra, c
           l = (l + ra.bias) * ea.invtau[col0 + jj];
           gj *= ea.tab->gscale[col0 + jj];              // 0 on greedy rows
           if (ea.mask != nullptr) {
-            const uint32_t lo = __shfl_sync(0xFFFFFFFFu, mw, jj), hi = __shfl_sync(0xFFFFFFFFu, mw, 16 + jj);
-            const uint32_t bits = wshift ? __funnelshift_r(lo, hi, wshift) : lo;
-            if (!((bits >> lane) & 1u)) l = -INFINITY;
+            // bit of row warp_v0 + lane sits in word (lane + wshift) >> 5 (lanes 0-15 / 16-31)
+            const uint32_t w = __shfl_sync(0xFFFFFFFFu, mw, msrc + jj);
+            if (!((w >> mbit) & 1u)) l = -INFINITY;
           }
         }
         if (isnan(l)) l = -INFINITY;

@@ -159,6 +159,7 @@ __device__ __forceinline__ void epi_tile_topk(uint32_t taddr, const RowArgs& ra,
                                               const TopkSmem& ts, int lane, int qd) {
   const int B = ea.B;
   const int wshift = ra.warp_v0 & 31;
+  const int msrc = ((lane + wshift) >> 5) << 4, mbit = (lane + wshift) & 31;
 #pragma unroll 1
   for (int g = qd; g * 8 < B; g += 2) {
     const int col0 = g * 8;
@@ -180,9 +181,9 @@ __device__ __forceinline__ void epi_tile_topk(uint32_t taddr, const RowArgs& ra,
       if (XFORM) {
         l = (l + ra.bias) * ea.invtau[col];
         if (ea.mask != nullptr) {
-          const uint32_t lo = __shfl_sync(0xFFFFFFFFu, mw, jj), hi = __shfl_sync(0xFFFFFFFFu, mw, 16 + jj);
-          const uint32_t bits = wshift ? __funnelshift_r(lo, hi, wshift) : lo;
-          if (!((bits >> lane) & 1u)) l = -INFINITY;
+          // bit of row warp_v0 + lane sits in word (lane + wshift) >> 5 (lanes 0-15 / 16-31)
+          const uint32_t w = __shfl_sync(0xFFFFFFFFu, mw, msrc + jj);
+          if (!((w >> mbit) & 1u)) l = -INFINITY;
         }
       }
       if (isnan(l)) l = -INFINITY;

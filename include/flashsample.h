@@ -82,8 +82,22 @@ const char* fs_last_error(void);
  * Fails with FS_ERR_UNSUPPORTED if the device is not compute capability 10.0 (B200). */
 fs_status fs_ctx_create(int device, fs_ctx** out);
 void fs_ctx_destroy(fs_ctx* ctx);
-/* Testing / tuning knobs: force the CUDA-core kernel (1) or the tcgen05 kernel (0, default);
- * cap the persistent grid at `max_ctas` (0 = number of SMs). */
+/* Options (name, value); unknown names -> FS_ERR_INVALID.
+ *   "fuse_reduce" (default 1): plain sampling (single group, no logZ / log-prob outputs) ends in
+ *       the stage-1 kernel: every CTA folds its candidate per row into a 64-bit atomicMax of
+ *       (order key << 32 | ~idx) in the context's workspace, and the last CTA to finish writes
+ *       idx_out / score_out (Alg. 2 stage 2, done in L2 instead of a second kernel).
+ *       0 = separate stage-2 reduce kernel.  Same results bit for bit.
+ *   "pdl_w" (default 0): launch stage 1 with programmatic dependent launch.  The kernel then starts
+ *       while the preceding kernel on the stream finishes and streams its first W tiles BEFORE
+ *       waiting for it; every other input (h, bias, temperature, mask, seeds, steps) is read and
+ *       every output written only after the wait.  Contract: W must not be written by the kernel
+ *       immediately preceding the call on the same stream (LM-head weights are read-only while
+ *       decoding).  Saves the launch gap and the pipeline fill of back-to-back decode steps.
+ *   Tuning / testing: "force_simt" (1 = CUDA-core kernel), "max_ctas" (cap the persistent grid,
+ *   0 = number of SMs), "pdl" (stage 1 -> stage 2 programmatic launch, default 1), "pair" (CTA-pair
+ *   kernel: -1 auto, 0 off, 1 on), "stages", "kbps", "unit_rows", "l2promo", "w_policy",
+ *   "topk_mode", "time_stage1" (below); "dbg_no_mma", "dbg_no_epi" (debug: results are garbage). */
 fs_status fs_ctx_set_option(fs_ctx* ctx, const char* name, int64_t value);
 /* Measurement hook (used by bench.py for the roofline figure).  With option "time_stage1" = 1
  * every call records a CUDA event pair around each stage-1 (fused kernel) launch on the call's

@@ -53,6 +53,9 @@ struct fs_ctx {
   int pair_min_bn = 32;            // auto: use the pair kernel from this MMA N upwards (measured)
   int topk_mode = 0;               // fused top-k: 0 auto, 1 candidate lists in the epilogue, 2 via raw logits
   int* topk_rowcnt = nullptr;      // [256] per-row candidate counters of the list route (kept at 0 between calls)
+  int fuse_reduce = 1;             // single-group sampling without log-mass: last CTA finalizes (no stage 2)
+  int pdl_w = 0;                   // stage 1 launched with PDL, W streamed before the dependency wait
+  unsigned long long* fin_buf = nullptr;   // [256] row maxima + [1] CTA counter, 0 between calls
   // f2 peer-memory exchange (fs_comm_window_*)
   char* comm_win = nullptr;        // this rank's window (cudaMalloc, exported by IPC)
   size_t comm_off_flags = 0, comm_off_acks = 0, comm_off_status = 0;
@@ -231,6 +234,15 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
     n_slots = (a.V + 127) / 128;
   }
   const fs::SlotLayout lay{n_slots, tc ? 0 : 1, G, a.V, max_seg, a.group_size, unit, pair ? 1 : 0};
+  // one-kernel finalize: the last stage-1 CTA reduces the per-CTA candidates (fs_epilogue.cuh
+  // finalize_last_cta) -- single group, no log-mass outputs
+  const bool fin = tc && ctx->fuse_reduce && !a.lse && a.group_size >= a.V && a.idx_out != nullptr;
+  if (fin && !ctx->fin_buf) {
+    e = cudaMalloc(&ctx->fin_buf, 257 * sizeof(unsigned long long));
+    if (e != cudaSuccess) return fail(FS_ERR_OOM, "finalize buffer cudaMalloc failed");
+    e = cudaMemset(ctx->fin_buf, 0, 257 * sizeof(unsigned long long));
+    if (e != cudaSuccess) return cuda_fail(e, "finalize buffer memset");
+  }
   const int chunk = 256;
   const int Bc_max = std::min(a.B, chunk);
   const size_t part_bytes = (size_t)n_slots * Bc_max * sizeof(fs::State);
@@ -285,6 +297,13 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
       CUtensorMap hmap;
       if ((st = make_map(ctx, &hmap, p.h, a.D, Bc, pair ? BN / 2 : BN)) != FS_OK) return st;
       p.wmaps = wmaps;
+      p.pdl_w = ctx->pdl_w && ctx->pdl && !ctx->time_stage1;
+      if (fin) {
+        p.fin_best = ctx->fin_buf;
+        p.fin_ctr = reinterpret_cast<unsigned int*>(ctx->fin_buf + 256);
+        p.idx_out = a.idx_out + r0;
+        p.score_out = a.score_out ? a.score_out + r0 : nullptr;
+      }
       if (pair) {
         e = fs::launch_fused_tc2(hmap, p, BN, a.lse, G, stream);
         if (e != cudaSuccess) return cuda_fail(e, "stage-1 tcgen05 pair kernel launch");
@@ -297,6 +316,7 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
       if (e != cudaSuccess) return cuda_fail(e, "stage-1 CUDA-core kernel launch");
     }
     if (ev_end) cudaEventRecord(ev_end, stream);
+    if (fin) continue;                        // stage 1 wrote idx / score
     e = fs::launch_reduce(part, part_group, lay, Bc, a.n_groups, a.idx_out ? a.idx_out + r0 : nullptr,
                           a.score_out ? a.score_out + r0 : nullptr, a.logZ_out ? a.logZ_out + r0 : nullptr,
                           a.groups_out ? a.groups_out + (size_t)r0 * a.n_groups : nullptr, stream,
@@ -508,6 +528,7 @@ void fs_ctx_destroy(fs_ctx* ctx) {
   }
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->topk_rowcnt) cudaFree(ctx->topk_rowcnt);
+  if (ctx->fin_buf) cudaFree(ctx->fin_buf);
   fs_comm_window_destroy(ctx);
   delete ctx;
 }
@@ -525,6 +546,8 @@ fs_status fs_ctx_set_option(fs_ctx* ctx, const char* name, int64_t value) {
   else if (!strcmp(name, "w_policy")) ctx->w_policy = (int)value;
   else if (!strcmp(name, "epi_sleep")) ctx->epi_sleep = (int)value;
   else if (!strcmp(name, "pair")) ctx->pair = (int)value;
+  else if (!strcmp(name, "fuse_reduce")) ctx->fuse_reduce = (int)value;
+  else if (!strcmp(name, "pdl_w")) ctx->pdl_w = (int)value;
   else if (!strcmp(name, "pair_min_bn")) ctx->pair_min_bn = (int)value;
   else if (!strcmp(name, "topk_mode")) {
     if (value < 0 || value > 2) return fail(FS_ERR_INVALID, "topk_mode must be 0 (auto), 1 (epilogue lists) or 2 (raw logits)");

@@ -367,6 +367,35 @@ __device__ __forceinline__ void flush_warp(State (&st)[NST], int lane, int B, St
   }
 }
 
+// One-kernel finalize (StageOneParams::fin_best).  The candidate order of state_merge (larger key,
+// then smaller id) is the unsigned order of (key << 32 | ~idx), so a 64-bit atomicMax per row
+// reduces the per-CTA candidates in L2 in any arrival order with the same result as stage 2.
+__device__ __forceinline__ unsigned long long pack_state(const State& s) {
+  return ((unsigned long long)s.key << 32) | (unsigned long long)(s.idx >= 0 ? ~(uint32_t)s.idx : 0u);
+}
+// Called by all `nthr` epilogue threads (ids et) of every CTA after their atomicMax calls: the last
+// CTA to arrive (threadFenceReduction pattern) converts the row maxima to (idx, score) exactly as
+// stage 2's to_summary does, and leaves fin_best / fin_ctr at 0 for the next call.
+__device__ __forceinline__ void finalize_last_cta(unsigned long long* best, unsigned int* ctr, int B,
+                                                  int32_t* idx_out, float* score_out, int et, int nthr,
+                                                  uint32_t bar_id, volatile int* flag) {
+  __threadfence();
+  sm100::named_bar_sync(bar_id, nthr);
+  if (et == 0) *flag = (atomicAdd(ctr, 1u) == gridDim.x - 1) ? 1 : 0;
+  sm100::named_bar_sync(bar_id, nthr);
+  if (*flag) {
+    __threadfence();
+    for (int b = et; b < B; b += nthr) {
+      const unsigned long long v = atomicExch(&best[b], 0ull);
+      const uint32_t key = (uint32_t)(v >> 32);
+      const bool defined = key > kKeyNegInf;
+      idx_out[b] = defined ? (int32_t)~(uint32_t)v : -1;
+      if (score_out) score_out[b] = defined ? key_to_float(key) : -INFINITY;
+    }
+    if (et == 0) atomicExch(ctr, 0u);
+  }
+}
+
 // Persistent-CTA vocabulary partition: CTA c of G owns rows [u*floor(c*U/G), u*floor((c+1)*U/G))
 // (U = ceil(V/u) units of u rows, u in {16, 32, 64, 128}), clipped to V.  No split-K: every
 // logit's fp32 sum is independent of G and of the partition.

@@ -93,12 +93,19 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
     sm100::fence_barrier_init();
   }
   if (warp == 1) sm100::tmem_alloc(tmem_slot, (uint32_t)p.tmem_cols);
-  if (XFORM) fill_rowtab<PRQ>(tab, p.B, p.temperature, p.seeds, p.steps, p.step, threadIdx.x, kThreadsTC);
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   sm100::pdl_launch_dependents();
+  if (warp != 0) {
+    // every input but W is read past the dependency wait (the producer defers only its h loads)
+    if (p.pdl_w) sm100::pdl_wait();
+    if (XFORM) {
+      fill_rowtab<PRQ>(tab, p.B, p.temperature, p.seeds, p.steps, p.step, threadIdx.x - 32, kThreadsTC - 32);
+      sm100::named_bar_sync(4, kThreadsTC - 32);
+    }
+  }
 
   int r0, r1;
   cta_rows(blockIdx.x, gridDim.x, p.V, p.unit_rows, r0, r1);
@@ -111,6 +118,22 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
       const uint64_t pol_w = p.w_policy ? sm100::policy_evict_first() : sm100::policy_evict_normal();
       const uint64_t pol_h = sm100::policy_evict_last();
       const uint32_t stage_tx = (uint32_t)(kWStageBytes + h_stage_bytes);   // full boxes, OOB counted
+      // PDL: the first S stages' W loads are issued before the dependency wait; their h loads
+      // (the stage barrier still expects those bytes) are deferred until it returns.
+      auto load_h = [&](int stg, int kb0, int nk) {
+        for (int j = 0; j < nk; ++j)
+          sm100::tma_load_2d(h_ring + ((size_t)stg * KBPS + j) * h_stage_bytes, &tmH, &full[stg],
+                             (kb0 + j) * kBlockK, 0, pol_h);
+      };
+      int pend[16];
+      int npend = 0;
+      bool waited = !p.pdl_w;
+      auto flush_pending = [&]() {
+        sm100::pdl_wait();
+        waited = true;
+        for (int i = 0; i < npend; ++i) load_h(pend[i] & 31, pend[i] >> 8, (pend[i] >> 5) & 7);
+        npend = 0;
+      };
       int stage = 0;
       uint32_t phase = 0;
       int seg = 0;
@@ -121,19 +144,27 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
           for (int kb0 = 0; kb0 < num_kb; kb0 += KBPS) {
             const int nk = min(KBPS, num_kb - kb0);
             sm100::mbar_wait(&empty[stage], phase ^ 1);
+            if (p.dbg_no_mma == 2) {            // debug: MMAs on stale tiles, no loads
+              sm100::mbar_arrive(&full[stage]);
+              if (++stage == S) { stage = 0; phase ^= 1; }
+              continue;
+            }
             sm100::mbar_arrive_expect_tx(&full[stage], stage_tx * nk);
-            for (int j = 0; j < nk; ++j) {
-              const int kb = kb0 + j;
+            for (int j = 0; j < nk; ++j)
               sm100::tma_load_2d(w_ring + ((size_t)stage * KBPS + j) * kWStageBytes, wm, &full[stage],
-                                 kb * kBlockK, t0 - a, pol_w);
-              sm100::tma_load_2d(h_ring + ((size_t)stage * KBPS + j) * h_stage_bytes, &tmH, &full[stage],
-                                 kb * kBlockK, 0, pol_h);
+                                 (kb0 + j) * kBlockK, t0 - a, pol_w);
+            if (waited) {
+              load_h(stage, kb0, nk);
+            } else {
+              pend[npend++] = stage | (nk << 5) | (kb0 << 8);
+              if (npend == S) flush_pending();
             }
             if (++stage == S) { stage = 0; phase ^= 1; }
           }
         }
         a = b;
       }
+      if (!waited) flush_pending();
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -151,7 +182,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
           sm100::tc_fence_after();
           const uint32_t d_tmem = tmem_base + (uint32_t)(buf * BN);
           for (int kb0 = 0; kb0 < num_kb; kb0 += KBPS) {
-            const int nk = p.dbg_no_mma ? 0 : min(KBPS, num_kb - kb0);
+            const int nk = p.dbg_no_mma == 1 ? 0 : min(KBPS, num_kb - kb0);
             sm100::mbar_wait(&full[stage], phase);
             sm100::tc_fence_after();
             for (int j = 0; j < nk; ++j) {
@@ -306,9 +337,17 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
         State m = scratch[bb];
 #pragma unroll
         for (int w = 1; w < kEpiWarps; ++w) m = state_merge(m, scratch[w * BN + bb]);
-        p.part[(size_t)blockIdx.x * p.B + bb] = m;              // compact: slot = CTA
+        if (p.fin_best) {
+          if (m.key != kKeyNone) atomicMax(&p.fin_best[bb], pack_state(m));
+        } else {
+          p.part[(size_t)blockIdx.x * p.B + bb] = m;            // compact: slot = CTA
+        }
       }
-      if (et == 0) p.part_group[blockIdx.x] = (r0 < r1) ? 0 : -1;
+      if (p.fin_best)
+        finalize_last_cta(p.fin_best, p.fin_ctr, p.B, p.idx_out, p.score_out, et, 32 * kEpiWarps, 1,
+                          reinterpret_cast<volatile int*>(scratch + kEpiWarps * BN));
+      else if (et == 0)
+        p.part_group[blockIdx.x] = (r0 < r1) ? 0 : -1;
     }
   }
 
@@ -378,8 +417,17 @@ cudaError_t launch_fused_tc(const CUtensorMap& hmap, const StageOneParams& p_in,
     if (e != cudaSuccess) return e;
     attr_set[variant] = true;
   }
-  kern<<<grid, kThreadsTC, smem, stream>>>(hmap, p);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreadsTC);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = p.pdl_w ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, hmap, p);
 }
 
 }  // namespace fs

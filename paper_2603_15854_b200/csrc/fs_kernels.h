@@ -30,7 +30,7 @@ struct StageOneParams {
   int stages;                 // TMA ring depth (TC kernel)
   int unit_rows;              // CTA range granularity in rows (TC kernel): 16, 32, 64 or 128
   int kbps;                   // 64-wide K slices per ring stage (TC kernel)
-  int dbg_no_mma;             // debug: stream operands through the ring without issuing MMAs
+  int dbg_no_mma;             // debug: 1 = stream operands without issuing MMAs; 2 = MMAs on stale smem, no loads
   int dbg_no_epi;             // debug: epilogue drains TMEM without computing
   int w_policy;               // 1: W TMA loads carry an L2 evict_first hint
   int epi_sleep;              // ns backoff while epilogue warps wait for an accumulator
@@ -49,6 +49,15 @@ struct StageOneParams {
   int topk_m;                 // mode 1: ceil(k / grid)
   float* mat_out;             // mode 2: [B][mat_ld] fp32 logits of the local rows
   int64_t mat_ld;
+  // One-kernel finalize (mode 0, single group, no log-mass): each CTA folds its merged candidate
+  // into fin_best[b] by a 64-bit atomicMax of (key << 32 | ~idx); the last CTA to finish (fin_ctr)
+  // writes idx_out / score_out and resets both, so no stage-2 launch follows.
+  unsigned long long* fin_best;   // [256], all 0 between calls; nullptr = write `part` for stage 2
+  unsigned int* fin_ctr;          // CTAs finished, 0 between calls
+  int32_t* idx_out;               // [B] of this chunk
+  float* score_out;               // [B] or nullptr
+  int pdl_w;                      // launched with PDL: W loads may precede griddepcontrol.wait;
+                                  // everything else (h, bias, tau, mask, seeds, outputs) follows it
 };
 
 

@@ -1,0 +1,134 @@
+"""GPU: the one-kernel finalize (the last stage-1 CTA reduces the per-CTA candidates through a
+64-bit atomicMax per row; no stage-2 launch) and PDL-launched stage 1 (W streamed before the
+dependency wait, every other input after it) give exactly the two-kernel results, and the
+oracle's (parity rule in tests/parity.py)."""
+import numpy as np
+import pytest
+import torch
+
+import synth
+from parity import check_flat, oracle_flat
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    import paper_2603_15854_b200 as fs
+
+OPTS = (("fuse_reduce", 1), ("pdl_w", 0), ("pdl", 1), ("pair", -1), ("max_ctas", 0))
+
+
+@pytest.fixture(autouse=True)
+def _reset_options():
+    yield
+    if torch.cuda.is_available():
+        for k, v in OPTS:
+            fs.set_option(k, v)
+
+
+def _gpu(wl):
+    return {k: (getattr(wl, k).cuda() if getattr(wl, k) is not None else None)
+            for k in ("h", "W", "bias", "temperature", "mask")}
+
+
+def _sample(g, wl, step, **kw):
+    idx, score = fs.sample(g["h"], g["W"], bias=g["bias"], temperature=g["temperature"], mask=g["mask"],
+                           seed=wl.seed, step=step, return_score=True, **kw)
+    torch.cuda.synchronize()
+    return idx.cpu().numpy(), score.cpu().numpy()
+
+
+@pytest.mark.parametrize("B", [1, 5, 32, 33, 100, 256, 300])
+@pytest.mark.parametrize("config", ["llama3_8b", "qwen25_7b"])
+def test_one_kernel_equals_two_kernels_and_oracle(B, config):
+    wl = synth.make_workload(config, B, V=5000, D=256, seed_offset=7 * B)
+    g = _gpu(wl)
+    fs.set_option("fuse_reduce", 0)
+    i2, s2 = _sample(g, wl, 3)
+    fs.set_option("fuse_reduce", 1)
+    i1, s1 = _sample(g, wl, 3)
+    np.testing.assert_array_equal(i1, i2)
+    np.testing.assert_array_equal(s1.view(np.uint32), s2.view(np.uint32))
+    if B <= 33:
+        _, flat = oracle_flat(wl, 3)
+        check_flat(i1, s1, flat)
+
+
+@pytest.mark.parametrize("pair", [0, 1])
+def test_one_kernel_undefined_rows_and_many_calls(pair):
+    # edge pattern: one fully masked row (-> -1), one single-token row, per-row tau; 40 calls in a
+    # row must keep the finalize buffer / counter consistent (reset by the last CTA)
+    fs.set_option("pair", pair)
+    wl = synth.make_workload("qwen25_7b", 40, V=3000, D=128, pattern="edge", seed_offset=3)
+    g = _gpu(wl)
+    outs = []
+    for step in range(40):
+        outs.append(_sample(g, wl, step))
+    fs.set_option("fuse_reduce", 0)
+    for step in (0, 17, 39):
+        i2, s2 = _sample(g, wl, step)
+        np.testing.assert_array_equal(outs[step][0], i2)
+        np.testing.assert_array_equal(outs[step][1].view(np.uint32), s2.view(np.uint32))
+    _, flat = oracle_flat(wl, 17)
+    check_flat(outs[17][0], outs[17][1], flat)
+    assert (outs[17][0] == -1).any()
+
+
+@pytest.mark.parametrize("B", [8, 64])
+def test_pdl_w_respects_producer_kernels(B):
+    # Each call's h and temperature are written by a torch kernel IMMEDIATELY before the call on the
+    # same stream; with pdl_w the stage-1 kernel streams W before its dependency wait, so any read
+    # of h / tau before it would see stale values and change the sample.
+    wl = synth.make_workload("qwen25_7b", B, V=20000, D=512, seed_offset=B)
+    g = _gpu(wl)
+    h0, t0 = g["h"].clone(), g["temperature"].clone()
+    ref = []
+    for step in range(6):
+        g["h"].copy_(h0 * (1.0 + 0.25 * step))
+        g["temperature"].copy_(t0 * (1.0 + 0.1 * step))
+        ref.append(_sample(g, wl, step))
+    fs.set_option("pdl_w", 1)
+    got = []
+    for step in range(6):
+        g["h"].copy_(h0 * (1.0 + 0.25 * step))
+        g["temperature"].copy_(t0 * (1.0 + 0.1 * step))
+        idx, score = fs.sample(g["h"], g["W"], bias=g["bias"], temperature=g["temperature"], mask=g["mask"],
+                               seed=wl.seed, step=step, return_score=True)
+        got.append((idx, score))                       # no host sync between steps
+    torch.cuda.synchronize()
+    for (ir, sr), (ig, sg) in zip(ref, got):
+        np.testing.assert_array_equal(ir, ig.cpu().numpy())
+        np.testing.assert_array_equal(sr.view(np.uint32), sg.cpu().numpy().view(np.uint32))
+
+
+def test_pdl_w_back_to_back_full_size_and_graph():
+    # Llama-3-8B LM head, B=32: 20 back-to-back PDL calls into distinct outputs, then the same loop
+    # captured in a CUDA graph and replayed -- all equal the two-kernel results per step.
+    D, V, B = 4096, 128256, 32
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    W = (torch.randn(V, D, device="cuda", generator=gen) * 0.02).to(torch.bfloat16)
+    h = torch.randn(B, D, device="cuda", generator=gen).to(torch.bfloat16)
+    fs.set_option("fuse_reduce", 0)
+    ref = [fs.sample(h, W, seed=9, step=s) for s in range(20)]
+    torch.cuda.synchronize()
+    fs.set_option("fuse_reduce", 1)
+    fs.set_option("pdl_w", 1)
+    outs = [torch.empty(B, dtype=torch.int32, device="cuda") for _ in range(20)]
+    for s in range(20):
+        fs.sample(h, W, seed=9, step=s, out=outs[s])
+    torch.cuda.synchronize()
+    for s in range(20):
+        assert torch.equal(ref[s], outs[s]), s
+    stream = torch.cuda.Stream()
+    graph = torch.cuda.CUDAGraph()
+    for o in outs:
+        o.fill_(-7)
+    with torch.cuda.stream(stream):
+        fs.sample(h, W, seed=9, step=0, out=outs[0])      # warm-up on the capture stream
+        stream.synchronize()
+        with torch.cuda.graph(graph, stream=stream):
+            for s in range(20):
+                fs.sample(h, W, seed=9, step=s, out=outs[s])
+    graph.replay()
+    torch.cuda.synchronize()
+    for s in range(20):
+        assert torch.equal(ref[s], outs[s]), s

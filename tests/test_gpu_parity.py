@@ -33,7 +33,7 @@ def _run(wl, step, **kw):
 def _reset_options():
     yield
     if torch.cuda.is_available():
-        for k, v in (("force_simt", 0), ("max_ctas", 0), ("pdl", 1), ("stages", 0), ("pair", -1), ("kbps", 0)):
+        for k, v in (("force_simt", 0), ("max_ctas", 0), ("pdl", 1), ("stages", 0), ("pair", -1), ("kbps", 0), ("fuse_reduce", 1), ("pdl_w", 0)):
             fs.set_option(k, v)
 
 

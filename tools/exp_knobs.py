@@ -23,16 +23,22 @@ for B in Bs:
         try:
             for k, v in cfg.items():
                 fs.set_option(k, v)
-            t_end = time.time() + 0.3
-            while time.time() < t_end:
-                fn()
-            torch.cuda.synchronize()
+            with bench.ClockSampler(0) as cs:
+                t_end = time.time() + float(os.environ.get("KNOB_SECS", "1.0"))
+                while time.time() < t_end:
+                    for _ in range(20):
+                        fn()
+                    torch.cuda.synchronize()
+            smp = cs.samples[len(cs.samples) * 2 // 5:]
+            mhz = sorted(float(x[1][0]) for x in smp if x[1][0].replace(".", "").isdigit())
+            pw = sorted(float(x[1][2]) for x in smp if x[1][2].replace(".", "").isdigit())
+            clk = f"sm {mhz[len(mhz)//2] if mhz else -1:.0f} MHz {pw[len(pw)//2] if pw else -1:.0f} W"
             step = bench.time_loop(fn, 100, 5) * 1e3
             fs.set_option("time_stage1", 1); fs.query("stage1_ms")
             bench.time_loop(fn, 100, 5)
             t = fs.query("stage1_ms") / 100
             fs.set_option("time_stage1", 0)
-            print(f"B={B:3d} {cfg} step {step:8.2f} us stage1 {t*1e3:8.2f} us {2*V*D/(t*1e-3)/1e9:8.1f} GB/s", flush=True)
+            print(f"B={B:3d} {cfg} step {step:8.2f} us stage1 {t*1e3:8.2f} us {2*V*D/(t*1e-3)/1e9:8.1f} GB/s {clk}", flush=True)
         except Exception as e:
             fs.set_option("time_stage1", 0)
             print(f"B={B} {cfg} error {e}", flush=True)

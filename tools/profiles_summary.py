@@ -18,6 +18,9 @@ summary = {"command": "ncu --metrics gpu__time_duration.sum --clock-control none
            "note": "cold-cache, serialised per-launch times: compare shares, not absolutes", "kernels": out}
 if st1 and st2:
     summary["stage1_share_of_step"] = st1[0]["mean_ns"] / (st1[0]["mean_ns"] + st2[0]["mean_ns"])
+elif st1:
+    summary["stage1_share_of_step"] = 1.0
+    summary["note_one_kernel"] = "plain sampling is one fused kernel per step (fuse_reduce): no stage-2 launch"
 json.dump(summary, open(f"profiles/{rnd}/launches_b32_summary.json", "w"), indent=1)
 keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_sector_hit_rate.pct",
         "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",

@@ -55,6 +55,7 @@ struct fs_ctx {
   int* topk_rowcnt = nullptr;      // [256] per-row candidate counters of the list route (kept at 0 between calls)
   int fuse_reduce = 1;             // single-group sampling without log-mass: last CTA finalizes (no stage 2)
   int pdl_w = 0;                   // stage 1 launched with PDL, W streamed before the dependency wait
+  unsigned long long* dbg_times = nullptr;   // debug: per-CTA timeline of the fused kernels (tools/exp_times.py)
   unsigned long long* fin_buf = nullptr;   // [256] row maxima + [1] CTA counter, 0 between calls
   // f2 peer-memory exchange (fs_comm_window_*)
   char* comm_win = nullptr;        // this rank's window (cudaMalloc, exported by IPC)
@@ -283,6 +284,7 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
       // W row per request; measured on B200).
       p.dbg_no_mma = ctx->dbg_no_mma;
       p.dbg_no_epi = ctx->dbg_no_epi;
+      p.dbg_times = ctx->dbg_times;
       p.w_policy = ctx->w_policy;
       p.epi_sleep = ctx->epi_sleep;
       auto stages_for = [&](int k) { return pair ? fs::tc2_stages(BN, k) : fs::tc_stages(BN, k); };
@@ -548,6 +550,7 @@ fs_status fs_ctx_set_option(fs_ctx* ctx, const char* name, int64_t value) {
   else if (!strcmp(name, "pair")) ctx->pair = (int)value;
   else if (!strcmp(name, "fuse_reduce")) ctx->fuse_reduce = (int)value;
   else if (!strcmp(name, "pdl_w")) ctx->pdl_w = (int)value;
+  else if (!strcmp(name, "dbg_times")) ctx->dbg_times = reinterpret_cast<unsigned long long*>(value);
   else if (!strcmp(name, "pair_min_bn")) ctx->pair_min_bn = (int)value;
   else if (!strcmp(name, "topk_mode")) {
     if (value < 0 || value > 2) return fail(FS_ERR_INVALID, "topk_mode must be 0 (auto), 1 (epilogue lists) or 2 (raw logits)");

@@ -80,6 +80,12 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
+    if (p.dbg_times) {
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      p.dbg_times[blockIdx.x * 8 + 0] = sm100::globaltimer();
+      p.dbg_times[blockIdx.x * 8 + 4] = smid;
+    }
     sm100::prefetch_tmap(&tmH);
     for (int s = 0; s < p.max_seg; ++s) sm100::prefetch_tmap(&wmaps[s]);
     for (int s = 0; s < S; ++s) {
@@ -130,6 +136,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
       bool waited = !p.pdl_w;
       auto flush_pending = [&]() {
         sm100::pdl_wait();
+        if (p.dbg_times) p.dbg_times[blockIdx.x * 8 + 1] = sm100::globaltimer();
         waited = true;
         for (int i = 0; i < npend; ++i) load_h(pend[i] & 31, pend[i] >> 8, (pend[i] >> 5) & 7);
         npend = 0;
@@ -165,6 +172,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
         a = b;
       }
       if (!waited) flush_pending();
+      if (p.dbg_times) p.dbg_times[blockIdx.x * 8 + 2] = sm100::globaltimer();
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -325,6 +333,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
       // ring is free; use it as scratch to merge the 8 warps' candidates into ONE slot per CTA
       // (stage 2 then reads #CTA candidates per row instead of 8 x #CTA).
       sm100::named_bar_sync(1, 32 * kEpiWarps);
+      if (p.dbg_times && threadIdx.x == 64) p.dbg_times[blockIdx.x * 8 + 3] = sm100::globaltimer();
       State* scratch = reinterpret_cast<State*>(w_ring);        // [8][BN] <= 32 KB
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
@@ -348,6 +357,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
                           reinterpret_cast<volatile int*>(scratch + kEpiWarps * BN));
       else if (et == 0)
         p.part_group[blockIdx.x] = (r0 < r1) ? 0 : -1;
+      if (p.dbg_times && et == 0) p.dbg_times[blockIdx.x * 8 + 5] = sm100::globaltimer();
     }
   }
 

@@ -56,6 +56,8 @@ struct StageOneParams {
   unsigned int* fin_ctr;          // CTAs finished, 0 between calls
   int32_t* idx_out;               // [B] of this chunk
   float* score_out;               // [B] or nullptr
+  unsigned long long* dbg_times;  // debug: [grid][8] globaltimer ns (start, dependency wait done, last load
+                                  // issued, last tile drained), %smid, CTA done, 0, 0; or nullptr
   int pdl_w;                      // launched with PDL: W loads may precede griddepcontrol.wait;
                                   // everything else (h, bias, tau, mask, seeds, outputs) follows it
 };

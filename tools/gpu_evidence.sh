@@ -1,7 +1,7 @@
 # Evidence run on one B200: GPU tests, smoke, full bench (all configs), reference arm, ncu launch list,
-# ncu --set full summaries of the fused kernel at B = 1, 32, 256 (llama3_8b).
+# ncu --set full of the fused kernel at B = 1, 32, 256 (llama3_8b), compute-sanitizer.
 mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/gpu_info.csv
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw,power.limit --format=csv > gpurun_out/gpu_info.csv
 timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 900 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
 timeout 1200 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; tail -2 gpurun_out/bench.err
@@ -15,4 +15,5 @@ ncu -i gpurun_out/prof_b$B.ncu-rep --page details --csv > gpurun_out/prof_b$B.de
 ncu -i gpurun_out/prof_b$B.ncu-rep --page source --csv --print-source sass > gpurun_out/prof_b$B.source.csv 2>/dev/null
 rm -f gpurun_out/prof_b$B.ncu-rep
 done
-ls gpurun_out | head -30
+bash tools/gpu_sanitize.sh
+ls gpurun_out | head -40

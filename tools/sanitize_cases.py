@@ -9,8 +9,14 @@ wl = synth.make_workload("qwen25_7b", 40, V=3000, D=136, with_transforms=True)
 h, W, bias, tau, mask = (x.to(dev) for x in (wl.h, wl.W, wl.bias, wl.temperature, wl.mask))
 for pair in (0, 1):
     fs.set_option("pair", pair)
-    fs.sample(h, W, seed=1, step=2)
-    fs.sample(h, W, bias=bias, temperature=tau, mask=mask, seed=1, step=2, return_score=True)
+    for fuse, pdl_w in ((0, 0), (1, 0), (1, 1)):       # stage-2 kernel / one-kernel finalize / + PDL prefetch
+        fs.set_option("fuse_reduce", fuse)
+        fs.set_option("pdl_w", pdl_w)
+        for st in range(3):
+            fs.sample(h, W, seed=1, step=st)
+            fs.sample(h, W, bias=bias, temperature=tau, mask=mask, seed=1, step=2, return_score=True)
+    fs.set_option("fuse_reduce", 1)
+    fs.set_option("pdl_w", 0)
     fs.sample_grouped(h, W, group_size=512, bias=bias, temperature=tau, mask=mask, seed=1, step=2)
     fs.sample(h, W, seeds=torch.arange(40, device=dev), step=3, return_logprob=True)
     parts = [fs.sample_shard(h, W[a:b].contiguous(), a, 3000, seed=1, step=2).raw for a, b in ((0, 1500), (1500, 3000))]

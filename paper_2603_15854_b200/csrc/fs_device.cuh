@@ -33,8 +33,13 @@ __device__ __forceinline__ U4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c
   return U4{c0, c1, c2, c3};
 }
 
+// Word i (0..3, lane-dependent) of (x, y, z, w) with mask arithmetic (3 LOP3 + 2 masks): the
+// nested-ternary form compiled to divergent branches + warp reconvergence around the shuffles
+// that consume it (ncu: BSSY/BSYNC + branch_resolving stalls in the per-request epilogue).
 __device__ __forceinline__ uint32_t sel4(uint32_t x, uint32_t y, uint32_t z, uint32_t w, int i) {
-  return i == 0 ? x : i == 1 ? y : i == 2 ? z : w;
+  const uint32_t m1 = 0u - ((uint32_t)i & 1u), m2 = 0u - (((uint32_t)i >> 1) & 1u);
+  const uint32_t lo = (x & ~m1) | (y & m1), hi = (z & ~m1) | (w & m1);
+  return (lo & ~m2) | (hi & m2);
 }
 
 // Per-request draws (reading R18: key = seed_b, counter = (v >> 2, 2^31, step_b), word v & 3) of

@@ -52,8 +52,7 @@ __device__ __forceinline__ void fill_rowtab(RowTab* t, int B, const float* tempe
 // (v >> 2, 2^31, step_b) under key seed_b, word v & 3 (reading R18).
 __device__ __forceinline__ uint32_t per_request_bits(const RowTab* t, uint32_t v, int b) {
   const U4 o = philox4x32_10(v >> 2, 0x80000000u, t->c2[b], t->c3[b], t->k0[b], t->k1[b]);
-  const uint32_t sel = v & 3u;
-  return sel == 0 ? o.x : sel == 1 ? o.y : sel == 2 ? o.z : o.w;
+  return sel4(o.x, o.y, o.z, o.w, (int)(v & 3u));
 }
 
 struct EpiArgs {

@@ -259,6 +259,19 @@ fs_status fs_comm_window_destroy(fs_ctx* ctx);
 fs_status fs_merge_summaries(const fs_summary* a, const fs_summary* b, fs_summary* out,
                              int count, void* stream);
 
+/* fs_copy_async -- stage one step's inputs for the end-to-end path (a serving loop's
+ * host -> device copy of h [, temperature, mask]).  A kernel on `stream` copies `bytes` from
+ * `src` (pinned host memory, read over PCIe through its unified address, or device memory) to
+ * device memory `dst`; both 16-byte aligned.  With option "pdl_w" it is launched with
+ * programmatic dependent launch: it loads src before and stores dst only after the preceding
+ * kernel on the stream completes (that kernel may still be reading dst), and the next fs_sample
+ * may start streaming W while the copy runs.  Asynchronous; the caller keeps src alive and
+ * unchanged until the stream passes the copy.  FS_ERR_INVALID: NULL / misaligned pointers or a
+ * pageable (unregistered) host src.
+ * fs_sample writes idx_out / score_out with plain stores, so they may also point to pinned host
+ * memory (a device -> host write of B x 4 bytes from the last CTA, no separate copy). */
+fs_status fs_copy_async(fs_ctx* ctx, void* dst, const void* src, size_t bytes, void* stream);
+
 /* Diagnostics (used by the tests to pin the device RNG; not on the hot path).
  * fs_random_bits: r[i] = Philox draw for (b[i], v[i]) under (seed, step, tag) -- the exact
  *                 counter layout of the convention above.  All arrays device, length n.

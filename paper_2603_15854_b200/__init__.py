@@ -291,12 +291,45 @@ def gumbel_from_bits(r: torch.Tensor) -> torch.Tensor:
     return g
 
 
+def copy_async(dst, src):
+    """fs_copy_async: kernel copy of `src` (pinned host or device tensor) into the device tensor
+    `dst` on the current stream (PDL-chained with fs_sample when option pdl_w is set)."""
+    if not dst.is_cuda or not dst.is_contiguous() or not src.is_contiguous():
+        raise ValueError("copy_async: dst must be a contiguous device tensor, src contiguous")
+    if src.device.type == "cpu" and not src.is_pinned():
+        raise ValueError("copy_async: a host src must be pinned")
+    nbytes = src.numel() * src.element_size()
+    if dst.numel() * dst.element_size() != nbytes:
+        raise ValueError("copy_async: size mismatch")
+    _lib.check(_lib.lib().fs_copy_async(context(dst.device), _ptr(dst), _ptr(src), nbytes,
+                                        _stream(dst)), "fs_copy_async")
+
+
 def sample_from_host(h_host, W, *, temperature_host=None, mask_host=None, bias=None, seed=0, step=0,
                      h_dev=None, t_dev=None, m_dev=None, idx_dev=None, idx_host=None):
     """End-to-end call a serving loop makes: copy this step's inputs from (pinned) host memory,
     sample on the device, copy the sampled ids back.  Device staging buffers may be passed in
-    to avoid allocation.  Returns the host int32 [B] tensor."""
+    to avoid allocation.  Returns the host int32 [B] tensor.
+    With pinned host tensors the inputs are staged by fs_copy_async (a kernel, PDL-chained with
+    the sampling kernel) and the ids are written by the sampling kernel straight into the pinned
+    idx_host (no copy-engine round trips); otherwise torch copies are used."""
     dev = W.device
+    pinned = h_host.is_pinned() and (temperature_host is None or temperature_host.is_pinned()) and \
+        (mask_host is None or mask_host.is_pinned()) and (idx_host is None or idx_host.is_pinned())
+    if pinned:
+        h_dev = h_dev if h_dev is not None else torch.empty_like(h_host, device=dev)
+        copy_async(h_dev, h_host)
+        if temperature_host is not None:
+            t_dev = t_dev if t_dev is not None else torch.empty_like(temperature_host, device=dev)
+            copy_async(t_dev, temperature_host)
+        if mask_host is not None:
+            m_dev = m_dev if m_dev is not None else torch.empty_like(mask_host, device=dev)
+            copy_async(m_dev, mask_host)
+        idx_host = idx_host if idx_host is not None else torch.empty(h_host.shape[0], dtype=torch.int32,
+                                                                     pin_memory=True)
+        sample(h_dev, W, bias=bias, temperature=t_dev if temperature_host is not None else None,
+               mask=m_dev if mask_host is not None else None, seed=seed, step=step, out=idx_host)
+        return idx_host
     h_dev = h_dev if h_dev is not None else torch.empty_like(h_host, device=dev)
     h_dev.copy_(h_host, non_blocking=True)
     if temperature_host is not None:

@@ -838,6 +838,23 @@ fs_status fs_random_bits(uint64_t seed, uint64_t step, uint32_t tag, const int32
   return e == cudaSuccess ? FS_OK : cuda_fail(e, "random_bits launch");
 }
 
+fs_status fs_copy_async(fs_ctx* ctx, void* dst, const void* src, size_t bytes, void* stream) {
+  if (!ctx) return fail(FS_ERR_INVALID, "ctx is required");
+  if (bytes == 0) return FS_OK;
+  if (!dst || !src) return fail(FS_ERR_INVALID, "dst and src are required");
+  if ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15u)
+    return fail(FS_ERR_INVALID, "dst and src must be 16-byte aligned");
+  cudaPointerAttributes at{};
+  cudaError_t e = cudaPointerGetAttributes(&at, src);
+  if (e != cudaSuccess || (at.type != cudaMemoryTypeHost && at.type != cudaMemoryTypeDevice &&
+                           at.type != cudaMemoryTypeManaged))
+    return fail(FS_ERR_INVALID, "src must be pinned host memory or device memory");
+  e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  e = fs::launch_copy_in(dst, src, bytes, ctx->pdl_w && ctx->pdl, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? FS_OK : cuda_fail(e, "copy kernel launch");
+}
+
 fs_status fs_gumbel_from_bits(const uint32_t* r, float* g_out, int64_t n, void* stream) {
   if (n < 0 || (n > 0 && (!r || !g_out))) return fail(FS_ERR_INVALID, "r, g_out required");
   cudaError_t e = fs::launch_gumbel(r, g_out, n, static_cast<cudaStream_t>(stream));

@@ -138,5 +138,7 @@ cudaError_t launch_merge(const fs_summary* a, const fs_summary* b, fs_summary* o
 cudaError_t launch_random_bits(uint64_t seed, uint64_t step, uint32_t tag, const int32_t* b, const int64_t* v,
                                uint32_t* r, int64_t n, cudaStream_t stream);
 cudaError_t launch_gumbel(const uint32_t* r, float* g, int64_t n, cudaStream_t stream);
+// Input staging copy (fs_copy_async): src loads before, dst stores after the PDL dependency wait.
+cudaError_t launch_copy_in(void* dst, const void* src, size_t bytes, bool pdl, cudaStream_t stream);
 
 }  // namespace fs

@@ -8,6 +8,8 @@
 //  merge    Alg. A.3 online binary merge of two summaries, by max reuse.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "fs_device.cuh"
 #include "fs_epilogue.cuh"
 #include "fs_kernels.h"
@@ -329,6 +331,51 @@ cudaError_t launch_gumbel(const uint32_t* r, float* g, int64_t n, cudaStream_t s
   const int64_t blocks = (n + 255) / 256;
   gumbel_kernel<<<(unsigned)(blocks < 65535 * 16 ? blocks : 65535 * 16), 256, 0, stream>>>(r, g, n);
   return cudaGetLastError();
+}
+
+// Input staging for the end-to-end path (fs_copy_async): 16-byte loads of the source (pinned host
+// memory through UVA -- a PCIe read -- or device memory) are issued BEFORE the dependency wait, the
+// stores to dst only after it (the preceding kernel may still read dst, e.g. last step's h).
+// Launched with PDL: it triggers its dependents at once, so the next fused kernel's W prefetch
+// overlaps this copy.
+constexpr int kCopyThreads = 256;
+constexpr int kCopyPerThread = 4;   // 16-byte words per thread per pass
+__global__ void __launch_bounds__(kCopyThreads)
+copy_in_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src, int64_t n16, uint8_t* dst_tail,
+               const uint8_t* src_tail, int tail) {
+  sm100::pdl_launch_dependents();
+  const int64_t stride = (int64_t)gridDim.x * kCopyThreads;
+  int64_t i0 = (int64_t)blockIdx.x * kCopyThreads + threadIdx.x;
+  uint4 v[kCopyPerThread];
+#pragma unroll
+  for (int j = 0; j < kCopyPerThread; ++j)
+    if (i0 + j * stride < n16) v[j] = src[i0 + j * stride];
+  uint8_t tb = 0;
+  if (i0 < tail) tb = src_tail[i0];
+  sm100::pdl_wait();
+#pragma unroll
+  for (int j = 0; j < kCopyPerThread; ++j)
+    if (i0 + j * stride < n16) dst[i0 + j * stride] = v[j];
+  if (i0 < tail) dst_tail[i0] = tb;
+  for (int64_t i = i0 + kCopyPerThread * stride; i < n16; i += stride) dst[i] = src[i];
+}
+
+cudaError_t launch_copy_in(void* dst, const void* src, size_t bytes, bool pdl, cudaStream_t stream) {
+  const int64_t n16 = (int64_t)(bytes / 16);
+  const int tail = (int)(bytes % 16);
+  const int64_t per_block = (int64_t)kCopyThreads * kCopyPerThread;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(1024, (n16 + per_block - 1) / per_block));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kCopyThreads);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, copy_in_kernel, static_cast<uint4*>(dst), static_cast<const uint4*>(src), n16,
+                            static_cast<uint8_t*>(dst) + n16 * 16, static_cast<const uint8_t*>(src) + n16 * 16, tail);
 }
 
 }  // namespace fs

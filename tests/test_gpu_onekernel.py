@@ -132,3 +132,48 @@ def test_pdl_w_back_to_back_full_size_and_graph():
     torch.cuda.synchronize()
     for s in range(20):
         assert torch.equal(ref[s], outs[s]), s
+
+
+@pytest.mark.parametrize("nbytes", [16, 4096 + 16, 262144, 3 * 1048576 + 48])
+def test_copy_async_pinned_and_device(nbytes):
+    src = torch.randint(0, 256, (nbytes,), dtype=torch.uint8).pin_memory()
+    dst = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    fs.copy_async(dst, src)
+    torch.cuda.synchronize()
+    assert torch.equal(dst.cpu(), src)
+    dst2 = torch.empty_like(dst)
+    fs.set_option("pdl_w", 1)
+    fs.copy_async(dst2, dst)
+    torch.cuda.synchronize()
+    assert torch.equal(dst2, dst)
+
+
+def test_copy_async_rejects_pageable_and_misaligned():
+    dst = torch.empty(64, dtype=torch.uint8, device="cuda")
+    with pytest.raises(ValueError):
+        fs.copy_async(dst, torch.zeros(64, dtype=torch.uint8))          # pageable host memory
+    src = torch.zeros(80, dtype=torch.uint8).pin_memory()
+    with pytest.raises(fs._lib.FlashSampleError):
+        fs.copy_async(dst, src[1:65])                                  # misaligned source
+
+
+@pytest.mark.parametrize("pdl_w", [0, 1])
+def test_sample_from_host_equals_device_path(pdl_w):
+    # end-to-end path: inputs staged by the copy kernel, ids written by the sampling kernel straight
+    # into pinned host memory; each step's host inputs change and no host sync happens in between
+    fs.set_option("pdl_w", pdl_w)
+    wl = synth.make_workload("qwen25_7b", 24, V=20000, D=512, seed_offset=11)
+    g = _gpu(wl)
+    hs = [(wl.h * (1.0 + 0.2 * s)).to(wl.h.dtype).pin_memory() for s in range(5)]
+    ts = [(wl.temperature * (1.0 + 0.1 * s)).pin_memory() for s in range(5)]
+    m_host = wl.mask.pin_memory()
+    h_dev, t_dev, m_dev = torch.empty_like(g["h"]), torch.empty_like(g["temperature"]), torch.empty_like(g["mask"])
+    outs = [torch.empty(24, dtype=torch.int32).pin_memory() for _ in range(5)]
+    for s in range(5):
+        fs.sample_from_host(hs[s], g["W"], temperature_host=ts[s], mask_host=m_host, bias=g["bias"], seed=wl.seed,
+                            step=s, h_dev=h_dev, t_dev=t_dev, m_dev=m_dev, idx_host=outs[s])
+    torch.cuda.synchronize()
+    for s in range(5):
+        ref = fs.sample(hs[s].cuda(), g["W"], bias=g["bias"], temperature=ts[s].cuda(), mask=g["mask"],
+                        seed=wl.seed, step=s)
+        assert torch.equal(ref.cpu(), outs[s]), s

@@ -27,6 +27,7 @@ namespace {
 constexpr int kChunk = 4096;
 constexpr int kPerThread = kChunk / 256;
 constexpr int kMaxK = 1024;
+constexpr int kMaxSurv = 1024;   // chunk fast path: survivors sorted in shared memory
 
 template <typename T>
 __device__ __forceinline__ float ldv(const T* p) {
@@ -88,6 +89,23 @@ __device__ __forceinline__ void block_radix_select(const uint32_t* keys, const b
   take = krem;
 }
 
+__device__ __forceinline__ void bitonic_sort_desc(Cand* a, int n) {   // n power of two, key desc, idx asc
+  for (int size = 2; size <= n; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int j = i ^ stride;
+        if (j > i) {
+          const bool up = (i & size) == 0;
+          const Cand x = a[i], y = a[j];
+          const bool x_first = (x.key > y.key) || (x.key == y.key && (uint32_t)x.idx < (uint32_t)y.idx);
+          if (x_first != up) { a[i] = y; a[j] = x; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
 template <typename T, bool XFORM>
 __global__ void __launch_bounds__(256)
 topk_chunk_kernel(const T* __restrict__ logits, int64_t ld, const float* __restrict__ bias,
@@ -96,6 +114,8 @@ topk_chunk_kernel(const T* __restrict__ logits, int64_t ld, const float* __restr
   __shared__ uint32_t hist[258];
   __shared__ int scan[256];
   __shared__ int n_gt;
+  __shared__ uint32_t runmax[256];
+  __shared__ Cand surv[kMaxSurv];
   const int b = blockIdx.y, c = blockIdx.x;
   const int v0 = c * kChunk + threadIdx.x * kPerThread;
   float it = 1.0f;
@@ -151,9 +171,79 @@ topk_chunk_kernel(const T* __restrict__ logits, int64_t ld, const float* __restr
     nvalid += valid[i];
   }
   const int chunk_n = min(kChunk, V - c * kChunk);
+  const int kk = min(k, chunk_n);
+  Cand* out = cand + ((size_t)b * nchunk + c) * k;
+  if (kk <= 256) {
+    // Fast path: a lower bound of the chunk's kk-th key from the 256 run maxima (16 columns per
+    // thread): kk runs have a maximum >= T, so >= kk elements are >= T.  The survivors {key >= T}
+    // (typically ~kk) are sorted (key desc, id asc); the first kk are the chunk's top kk with the
+    // same boundary-tie rule as the radix path (smaller column first).
+    uint32_t rmax = 0u;
+#pragma unroll
+    for (int i = 0; i < kPerThread; ++i) rmax = (valid[i] && keys[i] + 1u > rmax) ? keys[i] + 1u : rmax;
+    runmax[threadIdx.x] = rmax;                    // key + 1: 0 marks a run with no valid column
+    if (threadIdx.x == 0) n_gt = 0;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      // warp 0: radix select (4 x 8-bit digits) of the kk-th largest of the 256 run maxima
+      const int lane = threadIdx.x;
+      uint32_t rv[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) rv[i] = runmax[lane * 8 + i];
+      uint32_t prefix = 0u, pmask = 0u;
+      int krem = kk;
+      for (int pass = 0; pass < 4; ++pass) {
+        const int shift = 24 - 8 * pass;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) hist[lane * 8 + i] = 0u;
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (rv[i] != 0u && (rv[i] & pmask) == prefix) atomicAdd(&hist[(rv[i] >> shift) & 255u], 1u);
+        __syncwarp();
+        if (lane == 0) { hist[256] = 0u; hist[257] = (uint32_t)krem; }   // fewer than krem: digit 0
+        __syncwarp();
+        warp_digit<true>(hist, krem, lane, hist + 256);
+        __syncwarp();
+        prefix |= hist[256] << shift;
+        pmask |= 255u << shift;
+        krem = (int)hist[257];
+        __syncwarp();
+      }
+      // prefix = the kk-th largest (key + 1); fewer than kk runs with valid columns: keep all
+      int nr = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) nr += rv[i] != 0u;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) nr += __shfl_xor_sync(0xFFFFFFFFu, nr, o);
+      if (lane == 0) hist[256] = nr >= kk ? prefix - 1u : 0u;
+    }
+    __syncthreads();
+    const uint32_t T = hist[256];
+    int mine = 0;
+#pragma unroll
+    for (int i = 0; i < kPerThread; ++i) mine += valid[i] && keys[i] >= T;
+    const int base = atomicAdd(&n_gt, mine);     // n_gt = survivor count after the barrier
+    __syncthreads();
+    const int ns = n_gt;
+    if (ns <= kMaxSurv) {
+      int at = base;
+#pragma unroll
+      for (int i = 0; i < kPerThread; ++i)
+        if (valid[i] && keys[i] >= T) surv[at++] = Cand{keys[i], v0 + i};
+      int npow = 1;
+      while (npow < ns) npow <<= 1;
+      for (int i = ns + (int)threadIdx.x; i < npow; i += 256) surv[i] = Cand{0u, 0x7FFFFFFF};
+      __syncthreads();
+      bitonic_sort_desc(surv, npow);
+      for (int j = threadIdx.x; j < k; j += 256) out[j] = j < kk ? surv[j] : Cand{kKeyNone, -1};
+      if (threadIdx.x == 0) slot_lb[(size_t)b * nchunk + c] = (m <= chunk_n) ? surv[m - 1].key : 0u;
+      return;
+    }
+    __syncthreads();                              // heavy ties: exact radix path below
+  }
   uint32_t Tk = 0;
   int take = 0;
-  const int kk = min(k, chunk_n);
   block_radix_select(keys, valid, kPerThread, kk, hist, Tk, take);
   // count ties (key == T) per thread in index order; exclusive scan over threads
   int ties = 0;
@@ -169,7 +259,6 @@ topk_chunk_kernel(const T* __restrict__ logits, int64_t ld, const float* __restr
     __syncthreads();
   }
   int tie_pos = scan[threadIdx.x] - ties;        // exclusive prefix
-  Cand* out = cand + ((size_t)b * nchunk + c) * k;
   const int n_greater = kk - take;
 #pragma unroll
   for (int i = 0; i < kPerThread; ++i) {
@@ -192,23 +281,6 @@ topk_chunk_kernel(const T* __restrict__ logits, int64_t ld, const float* __restr
     block_radix_select(keys, valid, kPerThread, m, hist, Tm, tm);
   }
   if (threadIdx.x == 0) slot_lb[(size_t)b * nchunk + c] = Tm;
-}
-
-__device__ __forceinline__ void bitonic_sort_desc(Cand* a, int n) {   // n power of two, key desc, idx asc
-  for (int size = 2; size <= n; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const int j = i ^ stride;
-        if (j > i) {
-          const bool up = (i & size) == 0;
-          const Cand x = a[i], y = a[j];
-          const bool x_first = (x.key > y.key) || (x.key == y.key && (uint32_t)x.idx < (uint32_t)y.idx);
-          if (x_first != up) { a[i] = y; a[j] = x; }
-        }
-      }
-      __syncthreads();
-    }
-  }
 }
 
 constexpr int kFinalThreads = 512;

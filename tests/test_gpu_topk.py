@@ -97,3 +97,22 @@ def test_topk_topp_chi_square_1e6():
     assert c[np.setdiff1d(np.arange(8), keep)].sum() == 0
     _, p = stats.chi_square(c, target)
     assert p > 1e-3
+
+
+@pytest.mark.parametrize("k", [1, 50, 256])
+def test_topk_heavy_ties_fallback(k):
+    # chunk fast path (k <= 256: threshold from run maxima, survivors sorted in shared memory) and its
+    # fallback to the exact radix select when > 1024 survivors tie at the threshold: all-equal row,
+    # coarsely quantised rows (thousands of equal values), and a plain row
+    B, V = 4, 20000
+    gen = torch.Generator().manual_seed(k)
+    lg = torch.randn(B, V, generator=gen)
+    lg[0] = 0.0
+    lg[1] = torch.round(lg[1] * 2.0) / 2.0
+    lg[2] = torch.round(lg[2])
+    idx, score, logZ, logprob = fs.sample_logits(lg.cuda(), seed=5, step=1, top_k=k, top_p=1.0, return_all=True)
+    sc = sampler.scores_from_logits(lg.numpy().astype(np.float32), seed=5, step=1)
+    res = sampler.topk_topp_sample(sc, k, 1.0)
+    _check(idx, score, res)
+    # ties at the k-th key go to the smaller ids: the all-equal row keeps ids 0..k-1
+    assert int(idx[0]) in set(range(k))

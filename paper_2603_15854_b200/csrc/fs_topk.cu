@@ -226,6 +226,27 @@ topk_chunk_kernel(const T* __restrict__ logits, int64_t ld, const float* __restr
     const int base = atomicAdd(&n_gt, mine);     // n_gt = survivor count after the barrier
     __syncthreads();
     const int ns = n_gt;
+    if (ns <= 256) {
+      // few survivors (the usual case): each finds its rank in (key desc, id asc) order directly
+      int at = base;
+#pragma unroll
+      for (int i = 0; i < kPerThread; ++i)
+        if (valid[i] && keys[i] >= T) surv[at++] = Cand{keys[i], v0 + i};
+      __syncthreads();
+      if ((int)threadIdx.x < ns) {
+        const Cand x = surv[threadIdx.x];
+        int rank = 0;
+        for (int j = 0; j < ns; ++j) {
+          const Cand y = surv[j];
+          rank += (y.key > x.key) || (y.key == x.key && y.idx < x.idx);
+        }
+        if (rank < kk) out[rank] = x;
+        if (rank == m - 1 && m <= chunk_n) slot_lb[(size_t)b * nchunk + c] = x.key;
+      }
+      for (int j = kk + (int)threadIdx.x; j < k; j += 256) out[j] = Cand{kKeyNone, -1};
+      if (threadIdx.x == 0 && m > chunk_n) slot_lb[(size_t)b * nchunk + c] = 0u;
+      return;
+    }
     if (ns <= kMaxSurv) {
       int at = base;
 #pragma unroll

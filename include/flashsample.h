@@ -79,7 +79,10 @@ const char* fs_status_str(fs_status s);
 const char* fs_last_error(void);
 
 /* Create a context bound to CUDA device `device` (workspace, tensor-map cache, SM count).
- * Fails with FS_ERR_UNSUPPORTED if the device is not compute capability 10.0 (B200). */
+ * Fails with FS_ERR_UNSUPPORTED if the device is not compute capability 10.0 (B200).
+ * A context owns one workspace (candidate buffers, the finalize maxima / counter, top-k lists):
+ * calls on one context must be ordered -- one stream at a time, or streams ordered by events.
+ * Use one context per concurrently sampling stream. */
 fs_status fs_ctx_create(int device, fs_ctx** out);
 void fs_ctx_destroy(fs_ctx* ctx);
 /* Options (name, value); unknown names -> FS_ERR_INVALID.

@@ -209,10 +209,11 @@ def sample_grouped(h, W, *, group_size: int, bias=None, temperature=None, mask=N
 
 
 def sample_logits(logits, *, bias=None, temperature=None, mask=None, seed: int = 0, step: int = 0,
-                  seeds=None, steps=None, top_k: int = 0, top_p: float = 1.0, return_all: bool = False):
+                  seeds=None, steps=None, top_k: int = 0, top_p: float = 1.0, return_all: bool = False,
+                  return_score: bool = False):
     """Standalone Gumbel-max over materialised logits [B, V] (bf16 or fp32, row stride may exceed V)
     (fs_sample_logits[_ex]).  top_k (1..1024) / top_p: exact top-k then nucleus sampling (R19).
-    Returns idx [B], or (idx, score, logZ, logprob) if return_all."""
+    Returns idx [B]; (idx, score) if return_score; (idx, score, logZ, logprob) if return_all."""
     if not logits.is_cuda or logits.dim() != 2 or logits.stride(1) != 1:
         raise ValueError("logits must be a 2-D CUDA tensor with unit column stride")
     B, V = logits.shape
@@ -229,7 +230,7 @@ def sample_logits(logits, *, bias=None, temperature=None, mask=None, seed: int =
     seeds = _u64(seeds, B, "seeds", dev)
     steps = _u64(steps, B, "steps", dev)
     idx = torch.empty(B, dtype=torch.int32, device=dev)
-    score = torch.empty(B, dtype=torch.float32, device=dev) if return_all else None
+    score = torch.empty(B, dtype=torch.float32, device=dev) if (return_all or return_score) else None
     logZ = torch.empty(B, dtype=torch.float32, device=dev) if return_all else None
     logprob = torch.empty(B, dtype=torch.float32, device=dev) if return_all else None
     args = _lib.SampleArgs(_ptr(bias), _ptr(temperature), _ptr(mask), seed & (2**64 - 1), step & (2**64 - 1),
@@ -237,7 +238,9 @@ def sample_logits(logits, *, bias=None, temperature=None, mask=None, seed: int =
                            int(top_k), float(top_p))
     _lib.check(_lib.lib().fs_sample_logits_ex(context(dev), code, _ptr(logits), logits.stride(0), B, V,
                                               ctypes.byref(args), _stream(logits)), "fs_sample_logits_ex")
-    return (idx, score, logZ, logprob) if return_all else idx
+    if return_all:
+        return idx, score, logZ, logprob
+    return (idx, score) if return_score else idx
 
 
 def sample_shard(h, W_shard, vocab_offset: int, V_total: int, *, bias_shard=None, temperature=None,

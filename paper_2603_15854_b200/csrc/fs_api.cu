@@ -93,6 +93,16 @@ fs_status ensure_ws(fs_ctx* ctx, size_t bytes) {
   return FS_OK;
 }
 
+// One-kernel finalize buffer: [256] row maxima + counter, zeroed once, left zeroed by every call.
+fs_status ensure_fin(fs_ctx* ctx) {
+  if (ctx->fin_buf) return FS_OK;
+  cudaError_t e = cudaMalloc(&ctx->fin_buf, 257 * sizeof(unsigned long long));
+  if (e != cudaSuccess) return fail(FS_ERR_OOM, "finalize buffer cudaMalloc failed");
+  e = cudaMemset(ctx->fin_buf, 0, 257 * sizeof(unsigned long long));
+  if (e != cudaSuccess) return cuda_fail(e, "finalize buffer memset");
+  return FS_OK;
+}
+
 fs_status make_map(fs_ctx* ctx, CUtensorMap* m, const void* base, int64_t inner, int64_t rows, int box_rows) {
   for (const auto& e : ctx->map_cache)
     if (e.k.base == base && e.k.inner == inner && e.k.rows == rows && e.k.box == box_rows &&
@@ -238,11 +248,9 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
   // one-kernel finalize: the last stage-1 CTA reduces the per-CTA candidates (fs_epilogue.cuh
   // finalize_last_cta) -- single group, no log-mass outputs
   const bool fin = tc && ctx->fuse_reduce && !a.lse && a.group_size >= a.V && a.idx_out != nullptr;
-  if (fin && !ctx->fin_buf) {
-    e = cudaMalloc(&ctx->fin_buf, 257 * sizeof(unsigned long long));
-    if (e != cudaSuccess) return fail(FS_ERR_OOM, "finalize buffer cudaMalloc failed");
-    e = cudaMemset(ctx->fin_buf, 0, 257 * sizeof(unsigned long long));
-    if (e != cudaSuccess) return cuda_fail(e, "finalize buffer memset");
+  if (fin) {
+    fs_status s0 = ensure_fin(ctx);
+    if (s0 != FS_OK) return s0;
   }
   const int chunk = 256;
   const int Bc_max = std::min(a.B, chunk);
@@ -660,9 +668,13 @@ static fs_status sample_logits_impl(fs_ctx* ctx, fs_dtype dtype, const void* log
   fs::State* part = static_cast<fs::State*>(ctx->ws);
   int* part_group = reinterpret_cast<int*>(static_cast<char*>(ctx->ws) + grp_off);
   const bool lse = logZ_out || logprob_out;
+  const bool fin = ctx->fuse_reduce && !lse && B <= 256;   // last block finalizes (no stage-2 launch)
+  if (fin && (st = ensure_fin(ctx)) != FS_OK) return st;
   e = fs::launch_logits_sample(dtype, logits, ld, bias, temperature, mask, ((int64_t)V + 31) / 32, B, V, seed, step,
-                               lse, nblk, part, part_group, stream_, seeds, steps);
+                               lse, nblk, part, part_group, stream_, seeds, steps, fin ? ctx->fin_buf : nullptr,
+                               fin ? reinterpret_cast<unsigned int*>(ctx->fin_buf + 256) : nullptr, idx_out, score_out);
   if (e != cudaSuccess) return cuda_fail(e, "logits sampler launch");
+  if (fin) return FS_OK;
   const fs::SlotLayout lay{nblk, 1, nblk, V, 1, V, 128, 0};
   e = fs::launch_reduce(part, part_group, lay, B, 1, idx_out, score_out, logZ_out, nullptr, stream_, ctx->pdl != 0,
                         logprob_out);

@@ -377,10 +377,10 @@ __device__ __forceinline__ unsigned long long pack_state(const State& s) {
 // stage 2's to_summary does, and leaves fin_best / fin_ctr at 0 for the next call.
 __device__ __forceinline__ void finalize_last_cta(unsigned long long* best, unsigned int* ctr, int B,
                                                   int32_t* idx_out, float* score_out, int et, int nthr,
-                                                  uint32_t bar_id, volatile int* flag) {
+                                                  uint32_t bar_id, volatile int* flag, unsigned n_ctas) {
   __threadfence();
   sm100::named_bar_sync(bar_id, nthr);
-  if (et == 0) *flag = (atomicAdd(ctr, 1u) == gridDim.x - 1) ? 1 : 0;
+  if (et == 0) *flag = (atomicAdd(ctr, 1u) == n_ctas - 1) ? 1 : 0;
   sm100::named_bar_sync(bar_id, nthr);
   if (*flag) {
     __threadfence();

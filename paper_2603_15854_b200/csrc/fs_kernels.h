@@ -100,7 +100,9 @@ cudaError_t launch_logits_sample(fs_dtype dtype, const void* logits, int64_t ld,
                                  const float* temperature, const uint32_t* mask, int64_t mask_words, int B, int V,
                                  uint64_t seed, uint64_t step, bool lse, int nblk, State* part, int* part_group,
                                  cudaStream_t stream, const uint64_t* seeds = nullptr,
-                                 const uint64_t* steps = nullptr);
+                                 const uint64_t* steps = nullptr, unsigned long long* fin_best = nullptr,
+                                 unsigned int* fin_ctr = nullptr, int32_t* idx_out = nullptr,
+                                 float* score_out = nullptr);
 int logits_sample_blocks(int B, int V);   // V blocks of the standalone sampler grid
 // Top-k / top-p over materialised logits: chunk candidates (workspace B*topk_chunks(V)*k*8 bytes)
 // then a per-row merge + top-p + Gumbel-max.

@@ -13,6 +13,7 @@
 #include <algorithm>
 
 #include "fs_device.cuh"
+#include "fs_epilogue.cuh"
 #include "fs_sm100.cuh"
 #include "fs_kernels.h"
 
@@ -41,8 +42,10 @@ logits_sample_kernel(const T* __restrict__ logits, int64_t ld, const float* __re
                      const float* __restrict__ temperature, const uint32_t* __restrict__ mask, int64_t mask_words,
                      int B, int V, int vpb, uint32_t k0, uint32_t k1, uint32_t c2, uint32_t c3, State* part,
                      int* part_group, const uint64_t* __restrict__ seeds, const uint64_t* __restrict__ steps,
-                     uint64_t step) {
+                     uint64_t step, unsigned long long* fin_best, unsigned int* fin_ctr, int32_t* idx_out,
+                     float* score_out) {
   __shared__ State red[8][4];
+  __shared__ int fin_flag;
   const int b0 = blockIdx.y * 4;
   const int v_begin = blockIdx.x * vpb, v_end = min(V, v_begin + vpb);
   float it[4], gsc[4];
@@ -141,7 +144,18 @@ logits_sample_kernel(const T* __restrict__ logits, int64_t ld, const float* __re
     State x = red[0][j];
 #pragma unroll
     for (int w = 1; w < 8; ++w) x = LSE ? state_merge(x, red[w][j]) : state_max(x, red[w][j]);
-    if (b < B) part[(size_t)blockIdx.x * B + b] = x;
+    if (b < B) {
+      if (!LSE && fin_best) {                   // one-kernel finalize (fs_epilogue.cuh)
+        if (x.key != kKeyNone) atomicMax(&fin_best[b], pack_state(x));
+      } else {
+        part[(size_t)blockIdx.x * B + b] = x;
+      }
+    }
+  }
+  if (!LSE && fin_best) {
+    finalize_last_cta(fin_best, fin_ctr, B, idx_out, score_out, threadIdx.x, 256, 1, &fin_flag,
+                      gridDim.x * gridDim.y);
+    return;
   }
   if (threadIdx.x == 0 && blockIdx.y == 0) part_group[blockIdx.x] = 0;
   sm100::pdl_launch_dependents();
@@ -152,7 +166,9 @@ logits_sample_kernel(const T* __restrict__ logits, int64_t ld, const float* __re
 cudaError_t launch_logits_sample(fs_dtype dtype, const void* logits, int64_t ld, const float* bias,
                                  const float* temperature, const uint32_t* mask, int64_t mask_words, int B, int V,
                                  uint64_t seed, uint64_t step, bool lse, int nblk, State* part, int* part_group,
-                                 cudaStream_t stream, const uint64_t* seeds, const uint64_t* steps) {
+                                 cudaStream_t stream, const uint64_t* seeds, const uint64_t* steps,
+                                 unsigned long long* fin_best, unsigned int* fin_ctr, int32_t* idx_out,
+                                 float* score_out) {
   const int vpb = ((V + nblk - 1) / nblk + 255) / 256 * 256;
   const dim3 grid((V + vpb - 1) / vpb, (B + 3) / 4);
   const bool xform = bias || temperature || mask || seeds;
@@ -162,7 +178,8 @@ cudaError_t launch_logits_sample(fs_dtype dtype, const void* logits, int64_t ld,
 #define FS_LAUNCH(T, X, L, P)                                                                                 \
   logits_sample_kernel<T, X, L, P><<<grid, 256, 0, stream>>>(static_cast<const T*>(logits), ld, bias, temperature, \
                                                              mask, mask_words, B, V, vpb, k0, k1, c2, c3, part,  \
-                                                             part_group, seeds, steps, step)
+                                                             part_group, seeds, steps, step, fin_best, fin_ctr, \
+                                                             idx_out, score_out)
 #define FS_DISPATCH(T)                                                                                         \
   if (prq) { if (lse) FS_LAUNCH(T, true, true, true); else FS_LAUNCH(T, true, false, true); }                  \
   else if (xform) { if (lse) FS_LAUNCH(T, true, true, false); else FS_LAUNCH(T, true, false, false); }          \

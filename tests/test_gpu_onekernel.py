@@ -177,3 +177,23 @@ def test_sample_from_host_equals_device_path(pdl_w):
         ref = fs.sample(hs[s].cuda(), g["W"], bias=g["bias"], temperature=ts[s].cuda(), mask=g["mask"],
                         seed=wl.seed, step=s)
         assert torch.equal(ref.cpu(), outs[s]), s
+
+
+@pytest.mark.parametrize("B", [1, 7, 64, 256, 300])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_logits_sampler_one_kernel_equals_two_kernels(B, dtype):
+    # fs_sample_logits: the last block finalizes (B <= 256) == the stage-2 reduce kernel, bit for bit
+    wl = synth.make_workload("qwen25_7b", B, V=9000, D=64, seed_offset=B)
+    lg = (wl.h.float() @ wl.W.float().t() * 3.0).to(dtype).cuda()
+    kw = dict(bias=wl.bias.cuda(), temperature=wl.temperature.cuda(), mask=wl.mask.cuda(), seed=wl.seed, step=4)
+    seeds = torch.arange(B, device="cuda", dtype=torch.int64) * 31 + 7
+    res = {}
+    for fuse in (0, 1):
+        fs.set_option("fuse_reduce", fuse)
+        res[fuse] = [fs.sample_logits(lg, return_score=True, **kw),
+                     fs.sample_logits(lg, seeds=seeds, return_score=True, **kw),
+                     fs.sample_logits(lg, return_all=True, **kw)[:2]]          # log-mass: stage 2 both times
+        torch.cuda.synchronize()
+    for (i0, s0), (i1, s1) in zip(res[0], res[1]):
+        assert torch.equal(i0, i1)
+        assert torch.equal(s0.view(torch.int32), s1.view(torch.int32))

@@ -422,8 +422,11 @@ def run_single(args):
             "gpu_launches": (1 if one_kernel else 2) * args.steps * ((B + 255) // 256),
             "e2e": {"value": round(e2e_ms * 1e3, 2), "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": B * 4,
-                    "path": "sample_from_host: pinned inputs staged by fs_copy_async (kernel, PDL-chained), "
-                            "ids stored by the sampling kernel into pinned host memory"}}
+                    "path": ("sample_from_host -> fs_sample_staged: the sampling kernel copies the pinned host h "
+                             "into device memory itself (per-CTA slices + grid counter) and stores the ids into "
+                             "pinned host memory -- one kernel per step" if m_host is None else
+                             "sample_from_host: pinned inputs staged by fs_copy_async (PDL-chained copy kernel), "
+                             "ids stored by the sampling kernel into pinned host memory")}}
     if not args.no_sweep:
         line["sweep"] = sweep(fs, name, pk, args)
         # the other BASELINE.json configs (same protocol): transforms, grouped, 70B LM head

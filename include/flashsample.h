@@ -122,6 +122,20 @@ fs_status fs_sample(fs_ctx* ctx, fs_dtype dtype,
                     uint64_t seed, uint64_t step, int B, int D, int V,
                     int32_t* idx_out, float* score_out, void* stream);
 
+/* fs_sample_staged -- fs_sample for a serving loop whose hidden states arrive in host memory:
+ * h_host [B,D] is pinned (page-locked) host memory, 16-byte aligned; h_dev is a device buffer of
+ * the same size that the call overwrites.  On the one-kernel tcgen05 path (bf16, D % 8 == 0,
+ * option "fuse_reduce" on) the sampling kernel stages h itself: every CTA copies its slice of
+ * h_host into h_dev over PCIe after the dependency wait, a grid-wide counter orders the slices
+ * before the first h load, and W streaming starts meanwhile -- no copy kernel, no copy engine.
+ * Otherwise fs_copy_async stages h before fs_sample.  The grid barrier needs all (#SMs)
+ * persistent CTAs co-resident, which holds unless the GPU is shared (MPS / green contexts).
+ * idx_out / score_out may also be pinned host memory (see fs_copy_async).  Results equal
+ * fs_sample on the same h. */
+fs_status fs_sample_staged(fs_ctx* ctx, fs_dtype dtype, const void* h_host, void* h_dev, const void* W,
+                           const float* bias, const float* temperature, const uint32_t* mask, uint64_t seed,
+                           uint64_t step, int B, int D, int V, int32_t* idx_out, float* score_out, void* stream);
+
 /* fs_sample_grouped -- grouped / online FlashSampling with per-group log-mass summaries
  * (Group-Gumbel-Max §4.1, Alg. A.2/A.3 P:768-815, log-normalizer App. E).
  * Groups are contiguous vocabulary ranges G_k = [k*g, min((k+1)*g, V)), k = 0..ceil(V/g)-1,

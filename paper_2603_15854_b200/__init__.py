@@ -319,6 +319,22 @@ def sample_from_host(h_host, W, *, temperature_host=None, mask_host=None, bias=N
     dev = W.device
     pinned = h_host.is_pinned() and (temperature_host is None or temperature_host.is_pinned()) and \
         (mask_host is None or mask_host.is_pinned()) and (idx_host is None or idx_host.is_pinned())
+    if pinned and mask_host is None and h_host.dtype == torch.bfloat16:
+        # fs_sample_staged: the sampling kernel stages h itself (one kernel per step); the tiny
+        # temperature vector is read by the kernel straight from pinned host memory
+        h_dev = h_dev if h_dev is not None else torch.empty_like(h_host, device=dev)
+        idx_host = idx_host if idx_host is not None else torch.empty(h_host.shape[0], dtype=torch.int32,
+                                                                     pin_memory=True)
+        B, D = h_host.shape
+        V = W.shape[0]
+        if temperature_host is not None and (temperature_host.dtype != torch.float32 or temperature_host.numel() != B):
+            raise ValueError("temperature must be fp32 [B]")
+        if bias is not None and (bias.dtype != torch.float32 or bias.numel() != V or not bias.is_cuda):
+            raise ValueError("bias must be a device fp32 [V] tensor")
+        _lib.check(_lib.lib().fs_sample_staged(context(dev), FS_BF16, _ptr(h_host), _ptr(h_dev), _ptr(W), _ptr(bias),
+                                               _ptr(temperature_host), None, seed & (2**64 - 1), step & (2**64 - 1),
+                                               B, D, V, _ptr(idx_host), None, _stream(W)), "fs_sample_staged")
+        return idx_host
     if pinned:
         h_dev = h_dev if h_dev is not None else torch.empty_like(h_host, device=dev)
         copy_async(h_dev, h_host)

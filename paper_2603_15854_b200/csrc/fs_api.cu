@@ -93,12 +93,13 @@ fs_status ensure_ws(fs_ctx* ctx, size_t bytes) {
   return FS_OK;
 }
 
-// One-kernel finalize buffer: [256] row maxima + counter, zeroed once, left zeroed by every call.
+// One-kernel finalize buffer: [256] row maxima, CTA counter, staging barrier; zeroed once, left
+// zeroed by every call.
 fs_status ensure_fin(fs_ctx* ctx) {
   if (ctx->fin_buf) return FS_OK;
-  cudaError_t e = cudaMalloc(&ctx->fin_buf, 257 * sizeof(unsigned long long));
+  cudaError_t e = cudaMalloc(&ctx->fin_buf, 258 * sizeof(unsigned long long));
   if (e != cudaSuccess) return fail(FS_ERR_OOM, "finalize buffer cudaMalloc failed");
-  e = cudaMemset(ctx->fin_buf, 0, 257 * sizeof(unsigned long long));
+  e = cudaMemset(ctx->fin_buf, 0, 258 * sizeof(unsigned long long));
   if (e != cudaSuccess) return cuda_fail(e, "finalize buffer memset");
   return FS_OK;
 }
@@ -204,6 +205,7 @@ struct PathArgs {
   float* logprob_out;
   const uint64_t* seeds = nullptr;
   const uint64_t* steps = nullptr;
+  const void* h_host = nullptr;   // fs_sample_staged: pinned host h, staged into h by the kernel
 };
 
 // time_stage1 option: record a start event now and return the end event to record after stage 1.
@@ -313,6 +315,10 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
         p.fin_ctr = reinterpret_cast<unsigned int*>(ctx->fin_buf + 256);
         p.idx_out = a.idx_out + r0;
         p.score_out = a.score_out ? a.score_out + r0 : nullptr;
+        if (a.h_host) {
+          p.h_host = static_cast<const char*>(a.h_host) + (size_t)r0 * a.D * esz;
+          p.h_bar = reinterpret_cast<unsigned int*>(ctx->fin_buf + 257);
+        }
       }
       if (pair) {
         e = fs::launch_fused_tc2(hmap, p, BN, a.lse, G, stream);
@@ -618,6 +624,31 @@ fs_status fs_sample(fs_ctx* ctx, fs_dtype dtype, const void* h, const void* W, c
   if (!idx_out) return fail(FS_ERR_INVALID, "idx_out is required");
   PathArgs a{dtype, h, W, bias, temperature, mask, ((int64_t)V + 31) / 32, seed, step, B, D, V, 0,
              ((V + 127) / 128) * 128, false, idx_out, score_out, nullptr, nullptr, 1, nullptr};
+  return run_path(ctx, a, static_cast<cudaStream_t>(stream));
+}
+
+fs_status fs_sample_staged(fs_ctx* ctx, fs_dtype dtype, const void* h_host, void* h_dev, const void* W,
+                           const float* bias, const float* temperature, const uint32_t* mask, uint64_t seed,
+                           uint64_t step, int B, int D, int V, int32_t* idx_out, float* score_out, void* stream) {
+  fs_status s = check_common(ctx, dtype, h_dev, W, B, D, V);
+  if (s != FS_OK) return s;
+  if (!idx_out || !h_host) return fail(FS_ERR_INVALID, "h_host and idx_out are required");
+  const size_t esz = dtype == FS_BF16 ? 2 : 4;
+  cudaPointerAttributes at{};
+  cudaError_t e = cudaPointerGetAttributes(&at, h_host);
+  if (e != cudaSuccess || at.type != cudaMemoryTypeHost)
+    return fail(FS_ERR_INVALID, "h_host must be pinned (page-locked) host memory");
+  if (reinterpret_cast<uintptr_t>(h_host) & 15u) return fail(FS_ERR_INVALID, "h_host must be 16-byte aligned");
+  // in-kernel staging needs the one-kernel tcgen05 path; otherwise the copy kernel stages h
+  const bool tc = !ctx->force_simt && dtype == FS_BF16 && (D % 8 == 0) && aligned16(h_dev) && aligned16(W);
+  PathArgs a{dtype, h_dev, W, bias, temperature, mask, ((int64_t)V + 31) / 32, seed, step, B, D, V, 0,
+             ((V + 127) / 128) * 128, false, idx_out, score_out, nullptr, nullptr, 1, nullptr};
+  if (tc && ctx->fuse_reduce) {
+    a.h_host = h_host;
+  } else {
+    s = fs_copy_async(ctx, h_dev, h_host, (size_t)B * D * esz, stream);
+    if (s != FS_OK) return s;
+  }
   return run_path(ctx, a, static_cast<cudaStream_t>(stream));
 }
 

@@ -377,7 +377,8 @@ __device__ __forceinline__ unsigned long long pack_state(const State& s) {
 // stage 2's to_summary does, and leaves fin_best / fin_ctr at 0 for the next call.
 __device__ __forceinline__ void finalize_last_cta(unsigned long long* best, unsigned int* ctr, int B,
                                                   int32_t* idx_out, float* score_out, int et, int nthr,
-                                                  uint32_t bar_id, volatile int* flag, unsigned n_ctas) {
+                                                  uint32_t bar_id, volatile int* flag, unsigned n_ctas,
+                                                  unsigned int* h_bar = nullptr) {
   __threadfence();
   sm100::named_bar_sync(bar_id, nthr);
   if (et == 0) *flag = (atomicAdd(ctr, 1u) == n_ctas - 1) ? 1 : 0;
@@ -391,8 +392,35 @@ __device__ __forceinline__ void finalize_last_cta(unsigned long long* best, unsi
       idx_out[b] = defined ? (int32_t)~(uint32_t)v : -1;
       if (score_out) score_out[b] = defined ? key_to_float(key) : -INFINITY;
     }
-    if (et == 0) atomicExch(ctr, 0u);
+    if (et == 0) {
+      atomicExch(ctr, 0u);
+      if (h_bar) atomicExch(h_bar, 0u);      // every CTA passed the staging barrier long ago
+    }
   }
+}
+
+// In-kernel input staging (StageOneParams::h_host): the `nthr` non-producer threads of every CTA
+// copy this CTA's slice of the pinned host h into the device h (past the dependency wait, so the
+// previous kernel no longer reads it), fence, and one thread arrives on the grid counter.
+__device__ __forceinline__ void stage_h_slice(const void* h_host, const void* h_dev, size_t bytes, int et, int nthr,
+                                              uint32_t bar_id, unsigned int* h_bar) {
+  const size_t n16 = bytes / 16;
+  const size_t per = (n16 + gridDim.x - 1) / gridDim.x;
+  const size_t lo = per * blockIdx.x, hi = min(n16, lo + per);
+  const uint4* src = static_cast<const uint4*>(h_host);
+  uint4* dst = static_cast<uint4*>(const_cast<void*>(h_dev));
+  for (size_t i = lo + et; i < hi; i += nthr) dst[i] = src[i];
+  if (blockIdx.x == 0)                       // bytes % 16 (D % 8 == 0 for bf16 makes this 0)
+    for (size_t i = n16 * 16 + et; i < bytes; i += nthr)
+      static_cast<uint8_t*>(const_cast<void*>(h_dev))[i] = static_cast<const uint8_t*>(h_host)[i];
+  __threadfence();
+  sm100::named_bar_sync(bar_id, nthr);
+  if (et == 0) atomicAdd(h_bar, 1u);
+}
+// Producer side: wait until every CTA staged its slice, then order the TMA reads after it.
+__device__ __forceinline__ void wait_h_staged(const unsigned int* h_bar) {
+  while (sm100::ld_acquire_gpu(h_bar) < gridDim.x) __nanosleep(64);
+  sm100::fence_proxy_async_global();
 }
 
 // Persistent-CTA vocabulary partition: CTA c of G owns rows [u*floor(c*U/G), u*floor((c+1)*U/G))

@@ -96,6 +96,8 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
       fill_rowtab<PRQ>(tab, p.B, p.temperature, p.seeds, p.steps, p.step, threadIdx.x - 32, kThreads - 32);
       sm100::named_bar_sync(4, kThreads - 32);
     }
+    if (p.h_host)
+      stage_h_slice(p.h_host, p.h, (size_t)p.B * p.D * 2, threadIdx.x - 32, kThreads - 32, 4, p.h_bar);
   }
 
   int r0, r1;
@@ -117,9 +119,10 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
       };
       int pend[16];
       int npend = 0;
-      bool waited = !p.pdl_w;
+      bool waited = !p.pdl_w && !p.h_host;      // h loads wait for the dependency / the staged h
       auto flush_pending = [&]() {
         sm100::pdl_wait();
+        if (p.h_host) wait_h_staged(p.h_bar);
         if (p.dbg_times) p.dbg_times[blockIdx.x * 8 + 1] = sm100::globaltimer();
         waited = true;
         for (int i = 0; i < npend; ++i) load_h(pend[i] & 31, pend[i] >> 8, (pend[i] >> 5) & 7);
@@ -277,7 +280,7 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
       }
       if (p.fin_best)
         finalize_last_cta(p.fin_best, p.fin_ctr, p.B, p.idx_out, p.score_out, et, 32 * kEpiWarps, 1,
-                          reinterpret_cast<volatile int*>(scratch + kSlotWarps * BN), gridDim.x);
+                          reinterpret_cast<volatile int*>(scratch + kSlotWarps * BN), gridDim.x, p.h_bar);
       else if (et == 0)
         p.part_group[blockIdx.x] = (r0 < r1) ? 0 : -1;
       if (p.dbg_times && et == 0) p.dbg_times[blockIdx.x * 8 + 5] = sm100::globaltimer();

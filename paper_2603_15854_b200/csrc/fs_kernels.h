@@ -58,6 +58,10 @@ struct StageOneParams {
   float* score_out;               // [B] or nullptr
   unsigned long long* dbg_times;  // debug: [grid][8] globaltimer ns (start, dependency wait done, last load
                                   // issued, last tile drained), %smid, CTA done, 0, 0; or nullptr
+  const void* h_host;             // in-kernel staging (fs_sample_staged): pinned host h copied into h by
+                                  // all CTAs after the dependency wait, then a grid barrier (h_bar)
+                                  // before the first h load; nullptr = h is already on the device
+  unsigned int* h_bar;            // grid-barrier counter (reset by the finalizing CTA)
   int pdl_w;                      // launched with PDL: W loads may precede griddepcontrol.wait;
                                   // everything else (h, bias, tau, mask, seeds, outputs) follows it
 };

@@ -197,3 +197,25 @@ def test_logits_sampler_one_kernel_equals_two_kernels(B, dtype):
     for (i0, s0), (i1, s1) in zip(res[0], res[1]):
         assert torch.equal(i0, i1)
         assert torch.equal(s0.view(torch.int32), s1.view(torch.int32))
+
+
+@pytest.mark.parametrize("B", [1, 32, 64, 300])
+@pytest.mark.parametrize("pdl_w", [0, 1])
+def test_sample_staged_in_kernel_equals_device_path(B, pdl_w):
+    # fs_sample_staged: every CTA copies its slice of the pinned host h into the device buffer after the
+    # dependency wait, a grid counter orders it before the first h load; temperature read from pinned
+    # host memory; ids written into pinned host memory.  5 steps with changing inputs, no host syncs.
+    fs.set_option("pdl_w", pdl_w)
+    wl = synth.make_workload("qwen25_7b", B, V=20000, D=512, seed_offset=13 + B)
+    W, bias = wl.W.cuda(), wl.bias.cuda()
+    hs = [(wl.h * (1.0 + 0.2 * s)).to(wl.h.dtype).pin_memory() for s in range(5)]
+    ts = [(wl.temperature * (1.0 + 0.1 * s)).pin_memory() for s in range(5)]
+    h_dev = torch.empty(hs[0].shape, dtype=hs[0].dtype, device="cuda")
+    outs = [torch.full((B,), -7, dtype=torch.int32).pin_memory() for _ in range(5)]
+    for s in range(5):
+        fs.sample_from_host(hs[s], W, temperature_host=ts[s], bias=bias, seed=wl.seed, step=s, h_dev=h_dev,
+                            idx_host=outs[s])
+    torch.cuda.synchronize()
+    for s in range(5):
+        ref = fs.sample(hs[s].cuda(), W, bias=bias, temperature=ts[s].cuda(), seed=wl.seed, step=s)
+        assert torch.equal(ref.cpu(), outs[s]), s

@@ -52,6 +52,7 @@ struct fs_ctx {
   int pair = -1;                   // CTA-pair kernel: -1 auto (by batch size), 0 off, 1 on
   int pair_min_bn = 32;            // auto: use the pair kernel from this MMA N upwards (measured)
   int topk_mode = 0;               // fused top-k: 0 auto, 1 candidate lists in the epilogue, 2 via raw logits
+  int topk_spans = 1;              // raw-logit route: span maxima + gather (1) or full chunk selection (0)
   int* topk_rowcnt = nullptr;      // [256] per-row candidate counters of the list route (kept at 0 between calls)
   int fuse_reduce = 1;             // single-group sampling without log-mass: last CTA finalizes (no stage 2)
   int pdl_w = 0;                   // stage 1 launched with PDL, W streamed before the dependency wait
@@ -376,7 +377,11 @@ fs_status run_topk_path(fs_ctx* ctx, const PathArgs& a, int k, float top_p, cuda
   // auto: lists for k <= 128 when the ring keeps >= 8 slices (measured: at k = 200 the
   // per-tile compactions cost more than the raw-logit round trip)
   const bool lists = ctx->topk_mode == 1 || (ctx->topk_mode == 0 && slices >= 8 && k <= 128);
-  if (lists && !ctx->topk_rowcnt) {
+  // raw-logit route with span maxima (stage 1 also writes per-32-row maxima; only the spans at or
+  // above the k-th largest are read back): needs the tcgen05 kernel and no bias / mask (the bound is
+  // taken on raw logits, valid under the monotone temperature transform)
+  const bool spans = !lists && tc && ctx->topk_spans && !a.bias && !a.mask && (a.V + 15) / 16 <= 32768;
+  if ((lists || spans) && !ctx->topk_rowcnt) {
     e = cudaMalloc(&ctx->topk_rowcnt, 256 * sizeof(int));
     if (e != cudaSuccess) return fail(FS_ERR_OOM, "row counter cudaMalloc failed");
     e = cudaMemset(ctx->topk_rowcnt, 0, 256 * sizeof(int));
@@ -390,14 +395,18 @@ fs_status run_topk_path(fs_ctx* ctx, const PathArgs& a, int k, float top_p, cuda
   }
   // workspace: candidates [Bc][G*k] (lists) or logits [Bc][V] fp32 + chunk candidates
   const int nslot = lists ? G : fs::topk_chunks(a.V);
-  const int stride = lists ? G * cap : nslot * k;            // candidates per row
+  const int stride = lists ? G * cap : spans ? a.V : nslot * k;   // candidates per row
   const size_t cand_bytes = (size_t)Bc_max * (stride * sizeof(fs::Cand) + nslot * sizeof(uint32_t));
   const size_t mat_off = (cand_bytes + 255) & ~size_t(255);
   const size_t mat_bytes = lists ? 0 : (size_t)Bc_max * a.V * sizeof(float);
-  fs_status st = ensure_ws(ctx, mat_off + mat_bytes);
+  const int64_t gld = ((int64_t)a.V + 15) / 16;
+  const size_t gmax_off = (mat_off + mat_bytes + 255) & ~size_t(255);
+  const size_t gmax_bytes = spans ? (size_t)Bc_max * gld * sizeof(uint32_t) : 0;
+  fs_status st = ensure_ws(ctx, gmax_off + gmax_bytes);
   if (st != FS_OK) return st;
   fs::Cand* cand = static_cast<fs::Cand*>(ctx->ws);
   float* mat = reinterpret_cast<float*>(static_cast<char*>(ctx->ws) + mat_off);
+  uint32_t* gmax = spans ? reinterpret_cast<uint32_t*>(static_cast<char*>(ctx->ws) + gmax_off) : nullptr;
   for (int r0 = 0; r0 < a.B; r0 += chunk) {
     const int Bc = std::min(chunk, a.B - r0);
     fs::StageOneParams p{};
@@ -427,6 +436,8 @@ fs_status run_topk_path(fs_ctx* ctx, const PathArgs& a, int k, float top_p, cuda
     p.topk_m = (k + G - 1) / G;
     p.mat_out = mat;
     p.mat_ld = a.V;
+    p.topk_gmax = gmax;
+    p.topk_gld = gld;
     cudaEvent_t ev_end = nullptr;
     if ((st = stage1_event(ctx, stream, &ev_end)) != FS_OK) return st;
     if (tc) {
@@ -468,11 +479,17 @@ fs_status run_topk_path(fs_ctx* ctx, const PathArgs& a, int k, float top_p, cuda
       e = fs::launch_topk_final(cand, stride, ctx->topk_rowcnt, Bc, k, top_p, p.temperature, a.seed, a.step, sd, stp,
                                 idx, sc, lz, lp, stream, r0, ctx->pdl != 0 && !ctx->time_stage1, p.topk_lb, G,
                                 p.topk_m);
-    else
+    else if (spans) {
+      e = fs::launch_topk_gather(mat, a.V, gmax, gld, p.temperature, Bc, a.V, k, cand, stride, ctx->topk_rowcnt,
+                                 stream);
+      if (e == cudaSuccess)
+        e = fs::launch_topk_final(cand, stride, ctx->topk_rowcnt, Bc, k, top_p, p.temperature, a.seed, a.step, sd,
+                                  stp, idx, sc, lz, lp, stream, r0, false, nullptr, 0, 1);
+    } else
       e = fs::launch_topk_sample(FS_F32, mat, a.V, a.bias, p.temperature, p.mask, a.mask_words, Bc, a.V, k, top_p,
                                  a.seed, a.step, sd, stp, cand, idx, sc, lz, lp, stream, r0);
     if (e != cudaSuccess) {
-      if (lists) cudaMemsetAsync(ctx->topk_rowcnt, 0, 256 * sizeof(int), stream);   // keep the counters valid
+      if (lists || spans) cudaMemsetAsync(ctx->topk_rowcnt, 0, 256 * sizeof(int), stream);   // keep the counters valid
       return cuda_fail(e, "top-k stage-2 launch");
     }
   }
@@ -563,6 +580,7 @@ fs_status fs_ctx_set_option(fs_ctx* ctx, const char* name, int64_t value) {
   else if (!strcmp(name, "epi_sleep")) ctx->epi_sleep = (int)value;
   else if (!strcmp(name, "pair")) ctx->pair = (int)value;
   else if (!strcmp(name, "fuse_reduce")) ctx->fuse_reduce = (int)value;
+  else if (!strcmp(name, "topk_spans")) ctx->topk_spans = (int)value;
   else if (!strcmp(name, "pdl_w")) ctx->pdl_w = (int)value;
   else if (!strcmp(name, "dbg_times")) ctx->dbg_times = reinterpret_cast<unsigned long long*>(value);
   else if (!strcmp(name, "pair_min_bn")) ctx->pair_min_bn = (int)value;

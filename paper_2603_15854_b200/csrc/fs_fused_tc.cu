@@ -268,7 +268,9 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
         sm100::tc_fence_after();
         const int row = t0 + 32 * q + lane;
         const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(set * BN);
-        epi_tile_store(taddr, row < min(b, t0 + kBlockM), row, p.B, p.mat_out, p.mat_ld);
+        const int span0 = t0 + 32 * q, t1 = min(b, t0 + kBlockM);
+        epi_tile_store(taddr, row < t1, row, p.B, p.mat_out, p.mat_ld, p.topk_gmax, p.topk_gld, span0 >> 4,
+                       max(0, min(32, t1 - span0)), lane);
         release_tmem(&tempty[set], 0, lane);
       }
       a = b;

@@ -49,6 +49,9 @@ struct StageOneParams {
   int topk_m;                 // mode 1: ceil(k / grid)
   float* mat_out;             // mode 2: [B][mat_ld] fp32 logits of the local rows
   int64_t mat_ld;
+  uint32_t* topk_gmax;        // mode 2 (optional): [B][gld] per 32-row warp span starting at row 16u:
+                              // max order_key(raw logit) at u, 1 at u+1 when the span has > 16 rows
+  int64_t topk_gld;           // ceil(V / 16)
   // One-kernel finalize (mode 0, single group, no log-mass): each CTA folds its merged candidate
   // into fin_best[b] by a 64-bit atomicMax of (key << 32 | ~idx); the last CTA to finish (fin_ctr)
   // writes idx_out / score_out and resets both, so no stage-2 launch follows.
@@ -108,6 +111,12 @@ cudaError_t launch_logits_sample(fs_dtype dtype, const void* logits, int64_t ld,
                                  unsigned int* fin_ctr = nullptr, int32_t* idx_out = nullptr,
                                  float* score_out = nullptr);
 int logits_sample_blocks(int B, int V);   // V blocks of the standalone sampler grid
+// Fused top-k raw-logit route with span maxima: per row, threshold = k-th largest span max (raw
+// space), gather the logits of the spans at or above it (transform: temperature only) into
+// cand[b][0, n_b), n_b -> row_count[b].  Then launch_topk_final (no slot bounds).
+cudaError_t launch_topk_gather(const float* mat, int64_t ld, const uint32_t* gmax, int64_t gld,
+                               const float* temperature, int B, int V, int k, Cand* cand, int64_t stride,
+                               int* row_count, cudaStream_t stream);
 // Top-k / top-p over materialised logits: chunk candidates (workspace B*topk_chunks(V)*k*8 bytes)
 // then a per-row merge + top-p + Gumbel-max.
 int topk_chunks(int V);

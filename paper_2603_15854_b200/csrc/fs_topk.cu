@@ -63,7 +63,7 @@ __device__ __forceinline__ void warp_digit(const uint32_t* hist, int krem, int l
   if (here) { out[0] = (uint32_t)d; out[1] = (uint32_t)nk; }
 }
 
-// Block-wide radix select over keys held by the calling threads (valid flags), 256 threads.
+// Block-wide radix select over keys held by the calling threads (valid flags), any multiple of 32 threads.
 // Returns (threshold T, number of elements equal to T to take) such that the k largest are
 // {key > T} plus `take` elements with key == T.  If fewer than k valid elements exist, T = 0
 // and take = #(key == 0) (i.e. everything).
@@ -78,7 +78,11 @@ __device__ __forceinline__ void block_radix_select(const uint32_t* keys, const b
     for (int i = 0; i < n; ++i)
       warp_hist_add(hist, valid[i] && (keys[i] & pmask) == prefix, (keys[i] >> shift) & 255u, threadIdx.x & 31);
     __syncthreads();
-    if (threadIdx.x < 32) warp_digit<true>(hist, krem, threadIdx.x, hist + 256);   // >= krem valid keys
+    if (threadIdx.x < 32) {
+      if (threadIdx.x == 0) { hist[256] = 0u; hist[257] = (uint32_t)krem; }   // fewer than krem: digit 0
+      __syncwarp();
+      warp_digit<true>(hist, krem, threadIdx.x, hist + 256);   // >= krem valid keys
+    }
     __syncthreads();
     prefix |= hist[256] << shift;
     pmask |= 255u << shift;
@@ -581,9 +585,85 @@ topk_final_kernel(const Cand* __restrict__ cand, int ncand, int* __restrict__ ro
   }
 }
 
+// Fused route with span maxima (stage 1 mode 2 + gmax): one block per row.  T = the k-th largest
+// of the threads' largest span maxima (k spans hold an element >= T, so the row's k-th largest raw
+// logit is >= T); relaxed by 8 key steps so that an element whose transformed value ties the k-th
+// after fp32 rounding of l/tau is still gathered.  Only the spans at or above it are read back.
+constexpr int kGatherThreads = 1024;
+constexpr int kGatherPer = 32;            // span entries per thread: V <= 16 * 1024 * 32
+__global__ void __launch_bounds__(kGatherThreads)
+topk_gather_kernel(const float* __restrict__ mat, int64_t ld, const uint32_t* __restrict__ gmax, int64_t gld,
+                   const float* __restrict__ temperature, int V, int k, Cand* __restrict__ cand, int64_t stride,
+                   int* __restrict__ row_count) {
+  __shared__ uint32_t hist[258];
+  __shared__ int cnt;
+  const int b = blockIdx.x;
+  const int64_t nunits = (V + 15) / 16;
+  const uint32_t* g = gmax + (int64_t)b * gld;
+  uint32_t keys[kGatherPer];
+  bool valid[kGatherPer];
+#pragma unroll
+  for (int j = 0; j < kGatherPer; ++j) {
+    const int64_t u = threadIdx.x + (int64_t)j * kGatherThreads;
+    keys[j] = u < nunits ? g[u] : 0u;
+    valid[j] = keys[j] > 1u;               // 0 / 1: no span starts at this unit
+  }
+  if (threadIdx.x == 0) cnt = 0;
+  // bound from the threads' maxima: k threads hold a span whose maximum is >= their k-th largest,
+  // so k elements are >= it (a 1-key-per-thread select instead of 32)
+  uint32_t tmax = 0u;
+#pragma unroll
+  for (int j = 0; j < kGatherPer; ++j) tmax = valid[j] && keys[j] > tmax ? keys[j] : tmax;
+  const bool tvalid = tmax > 1u;
+  uint32_t T = 0;
+  int take = 0;
+  block_radix_select(&tmax, &tvalid, 1, k, hist, T, take);   // T = 0 when fewer than k threads hold spans
+  const uint32_t Tr = T > 8u ? T - 8u : 0u;
+  float it = 1.0f;
+  if (temperature) {
+    const float t = temperature[b];
+    it = (t == 0.0f) ? 1.0f : (t > 0.0f && isfinite(t)) ? 1.0f / t : __int_as_float(0x7FC00000);
+  }
+  const float* row = mat + (int64_t)b * ld;
+  Cand* out = cand + (int64_t)b * stride;
+#pragma unroll 1
+  for (int j = 0; j < kGatherPer; ++j) {
+    if (!valid[j] || keys[j] < Tr) continue;
+    const int64_t u = threadIdx.x + (int64_t)j * kGatherThreads;
+    const int64_t v0 = u * 16;
+    const int64_t want = (u + 1 < nunits && g[u + 1] == 1u) ? 32 : 16;
+    const int n = (int)(want < V - v0 ? want : V - v0);
+    float x[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) x[i] = i < n ? row[v0 + i] : -INFINITY;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      if (i >= n) break;
+      float raw = x[i];
+      if (isnan(raw)) raw = -INFINITY;
+      if (order_key(raw) < Tr) continue;
+      float l = raw * it;
+      if (isnan(l)) l = -INFINITY;
+      const int pos = atomicAdd(&cnt, 1);
+      out[pos] = Cand{order_key(l), (int32_t)(v0 + i)};
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) row_count[b] = cnt;
+}
+
 }  // namespace
 
 int topk_chunks(int V) { return (V + kChunk - 1) / kChunk; }
+
+cudaError_t launch_topk_gather(const float* mat, int64_t ld, const uint32_t* gmax, int64_t gld,
+                               const float* temperature, int B, int V, int k, Cand* cand, int64_t stride,
+                               int* row_count, cudaStream_t stream) {
+  if ((int64_t)(V + 15) / 16 > (int64_t)kGatherThreads * kGatherPer) return cudaErrorInvalidValue;
+  topk_gather_kernel<<<B, kGatherThreads, 0, stream>>>(mat, ld, gmax, gld, temperature, V, k, cand, stride,
+                                                        row_count);
+  return cudaGetLastError();
+}
 int topk_max_k() { return kMaxK; }
 
 cudaError_t launch_topk_sample(fs_dtype dtype, const void* logits, int64_t ld, const float* bias,

@@ -258,7 +258,12 @@ __device__ __forceinline__ void topk_write_cols(const TopkSmem& ts, int B, int q
 
 // Raw-logit store (fallback when the candidate lists do not fit): this warp's 32 rows x all B
 // columns of one tile, acc (fp32, untransformed) -> out[b * ld + row]; coalesced per column.
-__device__ __forceinline__ void epi_tile_store(uint32_t taddr, bool valid, int row, int B, float* out, int64_t ld) {
+// gmax (optional): this warp's 32-row span starts at local row 16*u0 (span_rows valid rows, 0 =
+// empty span -> nothing written); per column the span's max order key of the raw logit goes to
+// gmax[col][u0] and the marker 1 to gmax[col][u0 + 1] when the span covers a second 16-row unit.
+__device__ __forceinline__ void epi_tile_store(uint32_t taddr, bool valid, int row, int B, float* out, int64_t ld,
+                                               uint32_t* gmax = nullptr, int64_t gld = 0, int64_t u0 = 0,
+                                               int span_rows = 0, int lane = 0) {
 #pragma unroll 1
   for (int col0 = 0; col0 < B; col0 += 8) {
     uint32_t r[8];
@@ -267,6 +272,18 @@ __device__ __forceinline__ void epi_tile_store(uint32_t taddr, bool valid, int r
 #pragma unroll
     for (int jj = 0; jj < 8; ++jj)
       if (valid && col0 + jj < B) out[(int64_t)(col0 + jj) * ld + row] = __uint_as_float(r[jj]);
+    if (gmax != nullptr && span_rows > 0) {
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        float x = __uint_as_float(r[jj]);
+        if (isnan(x)) x = -INFINITY;
+        const uint32_t km = __reduce_max_sync(0xFFFFFFFFu, valid ? order_key(x) : kKeyNone);
+        if (lane == jj && col0 + jj < B) {
+          gmax[(int64_t)(col0 + jj) * gld + u0] = km;
+          if (span_rows > 16) gmax[(int64_t)(col0 + jj) * gld + u0 + 1] = 1u;
+        }
+      }
+    }
   }
 }
 

@@ -28,6 +28,7 @@ def _reset():
         fs.set_option("topk_mode", 0)
         fs.set_option("force_simt", 0)
         fs.set_option("max_ctas", 0)
+        fs.set_option("topk_spans", 1)
 
 
 def _dev(t):
@@ -187,3 +188,36 @@ def test_topk_errors():
         fs.sample(_dev(wl.h), _dev(wl.W), top_k=2000)
     with pytest.raises(fs.FlashSampleError):
         fs.sample(_dev(wl.h), _dev(wl.W), top_p=0.5)                  # top_p needs top_k
+
+
+@pytest.mark.parametrize("B,V,k,p", [(1, 5000, 50, 0.95), (40, 20011, 50, 0.9), (256, 9000, 1, 1.0),
+                                     (7, 3001, 1024, 0.5), (33, 129, 64, 1.0)])
+def test_raw_route_span_gather_equals_chunk_selection(B, V, k, p):
+    # raw-logit route: span maxima written by stage 1 + gather of the spans at or above the k-th
+    # largest (topk_spans=1) vs the full chunk selection (topk_spans=0) -- identical results, with
+    # per-row temperature incl. a greedy row (tau = 0) and an invalid row (tau < 0)
+    fs.set_option("topk_mode", 2)
+    wl = synth.make_workload("llama3_8b", B, V=V, D=128, seed_offset=B + k, pattern="peaked")
+    tau = torch.rand(B, generator=torch.Generator().manual_seed(B)) + 0.5
+    if B > 2:
+        tau[1], tau[2] = 0.0, -1.0
+    out = {}
+    for spans in (0, 1):
+        fs.set_option("topk_spans", spans)
+        out[spans] = _run(wl, k, p, temperature=tau)
+    fs.set_option("topk_spans", 1)
+    for a, b in zip(out[0], out[1]):
+        assert torch.equal(a.view(torch.int32), b.view(torch.int32))
+    sc, res = _oracle(wl, k, p, temperature=tau)
+    _check(out[1][0], out[1][1], res)
+
+
+def test_raw_route_span_gather_all_ties():
+    # all-equal logits: every span reaches the threshold, the whole row is gathered; the k smallest
+    # ids are the top-k
+    fs.set_option("topk_mode", 2)
+    B, V, D, k = 3, 6000, 64, 37
+    h = torch.zeros(B, D, dtype=torch.bfloat16).cuda()
+    W = torch.zeros(V, D, dtype=torch.bfloat16).cuda()
+    idx = fs.sample(h, W, seed=1, step=2, top_k=k)
+    assert bool((idx.cpu() < k).all()) and bool((idx.cpu() >= 0).all())

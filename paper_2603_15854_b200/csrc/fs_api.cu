@@ -251,7 +251,10 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
   // one-kernel finalize: the last stage-1 CTA reduces the per-CTA candidates (fs_epilogue.cuh
   // finalize_last_cta) -- single group, no log-mass outputs
   const bool fin = tc && ctx->fuse_reduce && !a.lse && a.group_size >= a.V && a.idx_out != nullptr;
-  if (fin) {
+  // with log-mass outputs: the last CTA runs the per-row reduce itself (one warp per row; for small
+  // B, where a second kernel's launch + grid hop cost more than the serial rows)
+  const bool fin_lse = tc && ctx->fuse_reduce && a.lse && a.group_size >= a.V && a.B <= 16;   // measured crossover
+  if (fin || fin_lse) {
     fs_status s0 = ensure_fin(ctx);
     if (s0 != FS_OK) return s0;
   }
@@ -321,6 +324,15 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
           p.h_bar = reinterpret_cast<unsigned int*>(ctx->fin_buf + 257);
         }
       }
+      if (fin_lse) {
+        p.fin_lse = 1;
+        p.fin_ctr = reinterpret_cast<unsigned int*>(ctx->fin_buf + 256);
+        p.idx_out = a.idx_out ? a.idx_out + r0 : nullptr;
+        p.score_out = a.score_out ? a.score_out + r0 : nullptr;
+        p.logZ_out = a.logZ_out ? a.logZ_out + r0 : nullptr;
+        p.groups_out = a.groups_out ? a.groups_out + (size_t)r0 * a.n_groups : nullptr;
+        p.logprob_out = a.logprob_out ? a.logprob_out + r0 : nullptr;
+      }
       if (pair) {
         e = fs::launch_fused_tc2(hmap, p, BN, a.lse, G, stream);
         if (e != cudaSuccess) return cuda_fail(e, "stage-1 tcgen05 pair kernel launch");
@@ -333,7 +345,7 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
       if (e != cudaSuccess) return cuda_fail(e, "stage-1 CUDA-core kernel launch");
     }
     if (ev_end) cudaEventRecord(ev_end, stream);
-    if (fin) continue;                        // stage 1 wrote idx / score
+    if (fin || fin_lse) continue;             // stage 1 wrote the outputs
     e = fs::launch_reduce(part, part_group, lay, Bc, a.n_groups, a.idx_out ? a.idx_out + r0 : nullptr,
                           a.score_out ? a.score_out + r0 : nullptr, a.logZ_out ? a.logZ_out + r0 : nullptr,
                           a.groups_out ? a.groups_out + (size_t)r0 * a.n_groups : nullptr, stream,

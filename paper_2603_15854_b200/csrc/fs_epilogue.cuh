@@ -12,6 +12,7 @@
 // since -3.10 <= g <= 22.19, every l~ - M_w <= 3.1 and the max term is >= e^-22.2, so the
 // fp32 sum neither overflows nor underflows (reading R9).
 #pragma once
+#include "../../include/flashsample.h"
 #include "fs_device.cuh"
 #include "fs_sm100.cuh"
 
@@ -396,6 +397,74 @@ __device__ __forceinline__ void finalize_last_cta(unsigned long long* best, unsi
       atomicExch(ctr, 0u);
       if (h_bar) atomicExch(h_bar, 0u);      // every CTA passed the staging barrier long ago
     }
+  }
+}
+
+// Summary record of a state (Lemma P:254-270): M, I, L = M + log S; undefined -> (-inf, -1, -inf).
+__device__ __forceinline__ fs_summary to_summary(const State& s) {
+  fs_summary o;
+  const bool defined = s.key > kKeyNegInf;
+  o.max_score = defined ? key_to_float(s.key) : -INFINITY;
+  o.idx = defined ? s.idx : -1;
+  o.log_mass = (defined && s.S > 0.0f) ? o.max_score + logf(s.S) : -INFINITY;
+  return o;
+}
+
+// log p(idx) = l~_idx - logZ (App. E); -inf when the row is undefined.
+__device__ __forceinline__ float logprob_of(const State& s) {
+  const fs_summary f = to_summary(s);
+  return f.idx >= 0 && f.log_mass > -INFINITY ? __uint_as_float(s.lt) - f.log_mass : -INFINITY;
+}
+
+// Stage 2 of one batch row b (Alg. 2; App. E), one warp: lane L merges slots L, L+32, ...
+// (L2 loads, so a last CTA of the same grid may call it), then a fixed xor tree -- deterministic,
+// so logZ is bit-reproducible and identical whichever kernel runs it.
+__device__ __forceinline__ void reduce_row(const State* part, const int* part_group, int n_slots, int B, int b,
+                                           int lane, int32_t* idx_out, float* score_out, float* logZ_out,
+                                           fs_summary* groups_out, float* logprob_out) {
+  State acc = state_empty();
+#pragma unroll 4
+  for (int s = lane; s < n_slots; s += 32)
+    if (__ldcg(part_group + s) >= 0) {
+      const uint4 u = __ldcg(reinterpret_cast<const uint4*>(part + (size_t)s * B + b));
+      acc = state_merge(acc, State{u.x, (int32_t)u.y, __uint_as_float(u.z), u.w});
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    State other;
+    other.key = __shfl_xor_sync(0xFFFFFFFFu, acc.key, o);
+    other.idx = __shfl_xor_sync(0xFFFFFFFFu, acc.idx, o);
+    other.S = __shfl_xor_sync(0xFFFFFFFFu, acc.S, o);
+    other.lt = __shfl_xor_sync(0xFFFFFFFFu, acc.lt, o);
+    acc = (lane & o) ? state_merge(other, acc) : state_merge(acc, other);
+  }
+  if (lane == 0) {
+    const fs_summary f = to_summary(acc);
+    if (idx_out) idx_out[b] = f.idx;
+    if (score_out) score_out[b] = f.max_score;
+    if (logZ_out) logZ_out[b] = f.log_mass;
+    if (groups_out) groups_out[b] = f;
+    if (logprob_out) logprob_out[b] = logprob_of(acc);
+  }
+}
+
+// One-kernel finalize with log-mass (single group, small B): every CTA has written its candidate
+// slot (part, part_group); the last CTA to arrive runs stage 2's reduce_row for every row, one warp
+// per row, and resets the counter.
+__device__ __forceinline__ void finalize_lse_last_cta(const State* part, const int* part_group, int B,
+                                                      unsigned int* ctr, int32_t* idx_out, float* score_out,
+                                                      float* logZ_out, fs_summary* groups_out, float* logprob_out,
+                                                      int et, int nthr, uint32_t bar_id, volatile int* flag) {
+  __threadfence();
+  sm100::named_bar_sync(bar_id, nthr);
+  if (et == 0) *flag = (atomicAdd(ctr, 1u) == gridDim.x - 1) ? 1 : 0;
+  sm100::named_bar_sync(bar_id, nthr);
+  if (*flag) {
+    __threadfence();
+    const int w = et >> 5, nw = nthr >> 5, lane = et & 31;
+    for (int b = w; b < B; b += nw)
+      reduce_row(part, part_group, gridDim.x, B, b, lane, idx_out, score_out, logZ_out, groups_out, logprob_out);
+    if (et == 0) atomicExch(ctr, 0u);
   }
 }
 

@@ -362,6 +362,10 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
                           reinterpret_cast<volatile int*>(scratch + kEpiWarps * BN), gridDim.x, p.h_bar);
       else if (et == 0)
         p.part_group[blockIdx.x] = (r0 < r1) ? 0 : -1;
+      if (!p.fin_best && p.fin_lse)
+        finalize_lse_last_cta(p.part, p.part_group, p.B, p.fin_ctr, p.idx_out, p.score_out, p.logZ_out,
+                              p.groups_out, p.logprob_out, et, 32 * kEpiWarps, 1,
+                              reinterpret_cast<volatile int*>(scratch + kEpiWarps * BN));
       if (p.dbg_times && et == 0) p.dbg_times[blockIdx.x * 8 + 5] = sm100::globaltimer();
     }
   }

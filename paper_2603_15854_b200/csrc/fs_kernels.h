@@ -59,6 +59,11 @@ struct StageOneParams {
   unsigned int* fin_ctr;          // CTAs finished, 0 between calls
   int32_t* idx_out;               // [B] of this chunk
   float* score_out;               // [B] or nullptr
+  int fin_lse;                    // single group with log-mass, small B: the last CTA runs stage 2's
+                                  // per-row reduce over `part` (counter fin_ctr); outputs below
+  float* logZ_out;                // [B] or nullptr
+  fs_summary* groups_out;         // [B] (the single group's summary, e.g. a TP shard's) or nullptr
+  float* logprob_out;             // [B] or nullptr
   unsigned long long* dbg_times;  // debug: [grid][8] globaltimer ns (start, dependency wait done, last load
                                   // issued, last tile drained), %smid, CTA done, 0, 0; or nullptr
   const void* h_host;             // in-kernel staging (fs_sample_staged): pinned host h copied into h by

@@ -17,15 +17,6 @@
 
 namespace fs {
 
-__device__ __forceinline__ fs_summary to_summary(const State& s) {
-  fs_summary o;
-  const bool defined = s.key > kKeyNegInf;
-  o.max_score = defined ? key_to_float(s.key) : -INFINITY;
-  o.idx = defined ? s.idx : -1;
-  o.log_mass = (defined && s.S > 0.0f) ? o.max_score + logf(s.S) : -INFINITY;
-  return o;
-}
-
 __device__ __forceinline__ State from_summary(const fs_summary& m) {
   State s = state_empty();
   if (m.idx >= 0 && !(m.max_score == -INFINITY)) {
@@ -38,12 +29,6 @@ __device__ __forceinline__ State from_summary(const fs_summary& m) {
 
 constexpr int kReduceThreads = 256;
 
-// log p(idx) = l~_idx - logZ (App. E); -inf when the row is undefined.
-__device__ __forceinline__ float logprob_of(const State& s) {
-  const fs_summary f = to_summary(s);
-  return f.idx >= 0 && f.log_mass > -INFINITY ? __uint_as_float(s.lt) - f.log_mass : -INFINITY;
-}
-
 // Single group (Alg. 2 stage 2; or one TP shard's summary): one warp per batch row,
 // each lane merges slots lane, lane+32, ... (independent loads in flight), then a fixed
 // shuffle tree -- deterministic, so logZ is bit-reproducible.
@@ -55,27 +40,7 @@ reduce_rows_kernel(const State* __restrict__ part, const int* __restrict__ part_
   const int lane = threadIdx.x & 31;
   const int b = blockIdx.x * 4 + (threadIdx.x >> 5);
   if (b >= B) return;
-  State acc = state_empty();
-#pragma unroll 4
-  for (int s = lane; s < n_slots; s += 32)
-    if (part_group[s] >= 0) acc = state_merge(acc, part[(size_t)s * B + b]);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    State other;
-    other.key = __shfl_xor_sync(0xFFFFFFFFu, acc.key, o);
-    other.idx = __shfl_xor_sync(0xFFFFFFFFu, acc.idx, o);
-    other.S = __shfl_xor_sync(0xFFFFFFFFu, acc.S, o);
-    other.lt = __shfl_xor_sync(0xFFFFFFFFu, acc.lt, o);
-    acc = (lane & o) ? state_merge(other, acc) : state_merge(acc, other);
-  }
-  if (lane == 0) {
-    const fs_summary f = to_summary(acc);
-    if (idx_out) idx_out[b] = f.idx;
-    if (score_out) score_out[b] = f.max_score;
-    if (logZ_out) logZ_out[b] = f.log_mass;
-    if (groups_out) groups_out[b] = f;
-    if (logprob_out) logprob_out[b] = logprob_of(acc);
-  }
+  reduce_row(part, part_group, n_slots, B, b, lane, idx_out, score_out, logZ_out, groups_out, logprob_out);
 }
 
 // Grouped variant (§4.1, App. E): one block per batch row, one thread per group.  Slots are

@@ -219,3 +219,22 @@ def test_sample_staged_in_kernel_equals_device_path(B, pdl_w):
     for s in range(5):
         ref = fs.sample(hs[s].cuda(), W, bias=bias, temperature=ts[s].cuda(), seed=wl.seed, step=s)
         assert torch.equal(ref.cpu(), outs[s]), s
+
+
+@pytest.mark.parametrize("B", [1, 13, 16, 40])
+def test_one_kernel_log_mass_and_shard_equal_stage2(B):
+    # single group with logZ / log-prob (and a TP shard's summary): the last stage-1 CTA runs the
+    # per-row reduce (B <= 16; larger B keep the stage-2 kernel) -- bit-identical to the stage-2 kernel
+    wl = synth.make_workload("qwen25_7b", B, V=7001, D=256, seed_offset=5 * B)
+    g = _gpu(wl)
+    kw = dict(bias=g["bias"], temperature=g["temperature"], mask=g["mask"], seed=wl.seed, step=6)
+    out = {}
+    for fuse in (0, 1):
+        fs.set_option("fuse_reduce", fuse)
+        r = fs.sample(g["h"], g["W"], return_score=True, return_logprob=True, **kw)
+        sh = fs.sample_shard(g["h"], g["W"][2000:5000].contiguous(), 2000, 7001, bias_shard=g["bias"][2000:5000],
+                             temperature=g["temperature"], mask=g["mask"], seed=wl.seed, step=6)
+        torch.cuda.synchronize()
+        out[fuse] = list(r) + [sh.raw]
+    for a, b in zip(out[0], out[1]):
+        assert torch.equal(a.view(torch.int32), b.view(torch.int32))

@@ -52,7 +52,8 @@ struct fs_ctx {
   int pair = -1;                   // CTA-pair kernel: -1 auto (by batch size), 0 off, 1 on
   int pair_min_bn = 32;            // auto: use the pair kernel from this MMA N upwards (measured)
   int topk_mode = 0;               // fused top-k: 0 auto, 1 candidate lists in the epilogue, 2 via raw logits
-  int topk_spans = 1;              // raw-logit route: span maxima + gather (1) or full chunk selection (0)
+  int topk_spans = 1;
+  int grp_ranges = 1;              // grouped stage 2: host-computed group slot ranges (0 = device binary search)              // raw-logit route: span maxima + gather (1) or full chunk selection (0)
   int* topk_rowcnt = nullptr;      // [256] per-row candidate counters of the list route (kept at 0 between calls)
   int fuse_reduce = 1;             // single-group sampling without log-mass: last CTA finalizes (no stage 2)
   int pdl_w = 0;                   // stage 1 launched with PDL, W streamed before the dependency wait
@@ -74,6 +75,10 @@ struct fs_ctx {
   struct SegKey { const void* W; int64_t D; int V, G, unit, gs, promo; };
   struct SegEnt { SegKey k; CUtensorMap* dev; int max_seg; };
   std::vector<SegEnt> seg_cache;
+  // grouped stage 2: first candidate slot of every group ([n_groups + 1], device), per slot layout
+  struct GrpKey { int n_slots, simt, G, V, max_seg, gs, unit, pair; };
+  struct GrpEnt { GrpKey k; int* dev; };
+  std::vector<GrpEnt> grp_cache;
   int time_stage1 = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;   // created lazily
   size_t ev_used = 0;
@@ -91,6 +96,62 @@ fs_status ensure_ws(fs_ctx* ctx, size_t bytes) {
   cudaError_t e = cudaMalloc(&ctx->ws, want);
   if (e != cudaSuccess) return fail(FS_ERR_OOM, std::string("workspace cudaMalloc: ") + cudaGetErrorString(e));
   ctx->ws_bytes = want;
+  return FS_OK;
+}
+
+// Group slot ranges of a stage-1 slot layout (grouped stage 2): mirrors the part_group ids the
+// kernels write -- tcgen05: slot ((cta*max_seg + seg)*8 + warp) (pair: ((pair*max_seg + seg)*2 +
+// rank)*8 + warp) holds group a/gs of its segment, unused segments the CTA's last group; CUDA-core:
+// slot = 128-row tile.  Ids are non-decreasing, so lo[k] = first slot with id >= k.
+fs_status group_ranges(fs_ctx* ctx, const fs::SlotLayout& L, int n_groups, const int** out) {
+  for (const auto& e : ctx->grp_cache)
+    if (e.k.n_slots == L.n_slots && e.k.simt == L.simt && e.k.G == L.G && e.k.V == L.V && e.k.max_seg == L.max_seg &&
+        e.k.gs == L.group_size && e.k.unit == L.unit_rows && e.k.pair == L.pair) {
+      *out = e.dev;
+      return FS_OK;
+    }
+  std::vector<int> grp((size_t)L.n_slots, 0);
+  const int gs = L.group_size;
+  if (L.simt) {
+    for (int t = 0; t < L.n_slots; ++t) grp[t] = (t * 128) / gs;
+  } else {
+    const int units = L.pair ? L.G / 2 : L.G;
+    const int64_t U = (L.V + L.unit_rows - 1) / L.unit_rows;
+    for (int c = 0; c < units; ++c) {
+      const int r0 = (int)(L.unit_rows * ((int64_t)c * U / units));
+      const int r1 = (int)std::min<int64_t>(L.unit_rows * ((int64_t)(c + 1) * U / units), L.V);
+      int seg = 0;
+      auto put = [&](int sg, int g) {
+        for (int rk = 0; rk < (L.pair ? 2 : 1); ++rk)
+          for (int w = 0; w < 8; ++w) {
+            const int64_t slot = L.pair ? (((int64_t)c * L.max_seg + sg) * 2 + rk) * 8 + w
+                                        : ((int64_t)c * L.max_seg + sg) * 8 + w;
+            if (slot < L.n_slots) grp[slot] = g;
+          }
+      };
+      for (int a = r0; a < r1; ++seg) {
+        const int b = std::min(r1, (a / gs + 1) * gs);
+        put(seg, a / gs);
+        a = b;
+      }
+      const int last = (r1 > r0 ? r1 - 1 : r0) / gs;
+      for (; seg < L.max_seg; ++seg) put(seg, last);
+    }
+  }
+  std::vector<int> lo((size_t)n_groups + 1);
+  for (int k = 0; k <= n_groups; ++k)
+    lo[k] = (int)(std::lower_bound(grp.begin(), grp.end(), k) - grp.begin());
+  int* dev = nullptr;
+  cudaError_t e = cudaMalloc(&dev, lo.size() * sizeof(int));
+  if (e != cudaSuccess) return fail(FS_ERR_OOM, "group range cudaMalloc failed");
+  e = cudaMemcpy(dev, lo.data(), lo.size() * sizeof(int), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return cuda_fail(e, "group range copy");
+  if (ctx->grp_cache.size() >= 16) {
+    cudaFree(ctx->grp_cache.front().dev);
+    ctx->grp_cache.erase(ctx->grp_cache.begin());
+  }
+  ctx->grp_cache.push_back({{L.n_slots, L.simt, L.G, L.V, L.max_seg, gs, L.unit_rows, L.pair}, dev});
+  *out = dev;
   return FS_OK;
 }
 
@@ -346,10 +407,14 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
     }
     if (ev_end) cudaEventRecord(ev_end, stream);
     if (fin || fin_lse) continue;             // stage 1 wrote the outputs
+    const int* grp_lo = nullptr;
+    if (a.n_groups > 1 && ctx->grp_ranges && (st = group_ranges(ctx, lay, a.n_groups, &grp_lo)) != FS_OK)
+      return st;
     e = fs::launch_reduce(part, part_group, lay, Bc, a.n_groups, a.idx_out ? a.idx_out + r0 : nullptr,
                           a.score_out ? a.score_out + r0 : nullptr, a.logZ_out ? a.logZ_out + r0 : nullptr,
                           a.groups_out ? a.groups_out + (size_t)r0 * a.n_groups : nullptr, stream,
-                          ctx->pdl != 0 && !ctx->time_stage1, a.logprob_out ? a.logprob_out + r0 : nullptr);
+                          ctx->pdl != 0 && !ctx->time_stage1, a.logprob_out ? a.logprob_out + r0 : nullptr,
+                          grp_lo);
     if (e != cudaSuccess) return cuda_fail(e, "stage-2 reduce launch");
   }
   return FS_OK;
@@ -567,6 +632,7 @@ fs_status fs_ctx_create(int device, fs_ctx** out) {
 void fs_ctx_destroy(fs_ctx* ctx) {
   if (!ctx) return;
   for (auto& e : ctx->seg_cache) cudaFree(e.dev);
+  for (auto& e : ctx->grp_cache) cudaFree(e.dev);
   for (auto& pr : ctx->ev_pool) {
     cudaEventDestroy(pr.first);
     cudaEventDestroy(pr.second);
@@ -593,6 +659,7 @@ fs_status fs_ctx_set_option(fs_ctx* ctx, const char* name, int64_t value) {
   else if (!strcmp(name, "pair")) ctx->pair = (int)value;
   else if (!strcmp(name, "fuse_reduce")) ctx->fuse_reduce = (int)value;
   else if (!strcmp(name, "topk_spans")) ctx->topk_spans = (int)value;
+  else if (!strcmp(name, "grp_ranges")) ctx->grp_ranges = (int)value;
   else if (!strcmp(name, "pdl_w")) ctx->pdl_w = (int)value;
   else if (!strcmp(name, "dbg_times")) ctx->dbg_times = reinterpret_cast<unsigned long long*>(value);
   else if (!strcmp(name, "pair_min_bn")) ctx->pair_min_bn = (int)value;

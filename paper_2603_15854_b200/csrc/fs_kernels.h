@@ -106,7 +106,8 @@ struct SlotLayout {
 // Stage 2: reduce the candidate slots of every row into groups and the final sample.
 cudaError_t launch_reduce(const State* part, const int* part_group, const SlotLayout& lay, int B, int n_groups,
                           int32_t* idx_out, float* score_out, float* logZ_out, fs_summary* groups_out,
-                          cudaStream_t stream, bool pdl, float* logprob_out = nullptr);
+                          cudaStream_t stream, bool pdl, float* logprob_out = nullptr,
+                          const int* grp_lo = nullptr);   // [n_groups+1] first slot per group (host-computed)
 // Standalone sampler over materialised logits [B][ld] (bf16 or fp32): candidates per (V-block, row).
 cudaError_t launch_logits_sample(fs_dtype dtype, const void* logits, int64_t ld, const float* bias,
                                  const float* temperature, const uint32_t* mask, int64_t mask_words, int B, int V,

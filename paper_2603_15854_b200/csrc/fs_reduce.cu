@@ -68,13 +68,15 @@ __device__ __forceinline__ State shfl_xor_state(const State& a, int o) {
 __global__ void __launch_bounds__(kReduceThreads)
 reduce_groups_kernel(const State* __restrict__ part, const int* __restrict__ part_group, int n_slots, int B,
                      int n_groups, int32_t* idx_out, float* score_out, float* logZ_out, fs_summary* groups_out,
-                     float* logprob_out) {
+                     float* logprob_out, const int* __restrict__ grp_lo) {
   extern __shared__ int sg[];
   __shared__ State red[kReduceThreads];
   sm100::pdl_wait();
   const int b = blockIdx.x, tid = threadIdx.x;
-  for (int s = tid; s < n_slots; s += kReduceThreads) sg[s] = part_group[s];
-  __syncthreads();
+  if (!grp_lo) {                               // no precomputed ranges: stage the ids, binary search
+    for (int s = tid; s < n_slots; s += kReduceThreads) sg[s] = part_group[s];
+    __syncthreads();
+  }
   // 8 threads per group: thread `sub` merges slots lo+sub, lo+sub+8, ... (one batch of
   // independent loads), then a fixed xor-shuffle tree combines the 8 partial states.
   const int sub = tid & 7;
@@ -83,7 +85,8 @@ reduce_groups_kernel(const State* __restrict__ part, const int* __restrict__ par
     const int k = k0 + (tid >> 3);
     State g = state_empty();
     if (k < n_groups) {
-      const int lo = lower_bound_smem(sg, n_slots, k), hi = lower_bound_smem(sg, n_slots, k + 1);
+      const int lo = grp_lo ? grp_lo[k] : lower_bound_smem(sg, n_slots, k);
+      const int hi = grp_lo ? grp_lo[k + 1] : lower_bound_smem(sg, n_slots, k + 1);
       for (int s0 = lo + sub; s0 < hi; s0 += 64) {
         State v[8];
 #pragma unroll
@@ -156,7 +159,7 @@ __global__ void gumbel_kernel(const uint32_t* r, float* g, int64_t n) {
 
 cudaError_t launch_reduce(const State* part, const int* part_group, const SlotLayout& lay, int B, int n_groups,
                           int32_t* idx_out, float* score_out, float* logZ_out, fs_summary* groups_out,
-                          cudaStream_t stream, bool pdl, float* logprob_out) {
+                          cudaStream_t stream, bool pdl, float* logprob_out, const int* grp_lo) {
   cudaLaunchConfig_t cfg = {};
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -172,14 +175,14 @@ cudaError_t launch_reduce(const State* part, const int* part_group, const SlotLa
   }
   cfg.gridDim = dim3(B);
   cfg.blockDim = dim3(kReduceThreads);
-  cfg.dynamicSmemBytes = (size_t)lay.n_slots * sizeof(int);
+  cfg.dynamicSmemBytes = grp_lo ? 0 : (size_t)lay.n_slots * sizeof(int);
   if (cfg.dynamicSmemBytes > 40 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(reduce_groups_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)cfg.dynamicSmemBytes);
     if (e != cudaSuccess) return e;
   }
   return cudaLaunchKernelEx(&cfg, reduce_groups_kernel, part, part_group, lay.n_slots, B, n_groups, idx_out,
-                            score_out, logZ_out, groups_out, logprob_out);
+                            score_out, logZ_out, groups_out, logprob_out, grp_lo);
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -238,3 +238,26 @@ def test_one_kernel_log_mass_and_shard_equal_stage2(B):
         out[fuse] = list(r) + [sh.raw]
     for a, b in zip(out[0], out[1]):
         assert torch.equal(a.view(torch.int32), b.view(torch.int32))
+
+
+@pytest.mark.parametrize("opts", [{}, {"pair": 0}, {"pair": 1}, {"max_ctas": 37}, {"unit_rows": 64},
+                                  {"force_simt": 1}])
+@pytest.mark.parametrize("V,g,B", [(20011, 4096, 9), (9000, 128, 40), (5000, 640, 3)])
+def test_grouped_host_slot_ranges_equal_device_search(opts, V, g, B):
+    # grouped stage 2 with host-computed group slot ranges == the device binary search over the ids
+    # stage 1 wrote (every slot layout: 1-CTA, CTA pair, capped grid, coarse units, CUDA-core)
+    wl = synth.make_workload("qwen25_7b", B, V=V, D=128, seed_offset=V % 97 + B)
+    g_ = _gpu(wl)
+    for k, v in opts.items():
+        fs.set_option(k, v)
+    out = {}
+    for r in (0, 1):
+        fs.set_option("grp_ranges", r)
+        res = fs.sample_grouped(g_["h"], g_["W"], group_size=g, bias=g_["bias"], temperature=g_["temperature"],
+                                mask=g_["mask"], seed=wl.seed, step=2, return_groups=True)
+        torch.cuda.synchronize()
+        out[r] = [res[0], res[1], res[2], res[3].raw]
+    for k in ("grp_ranges", "force_simt", "unit_rows"):
+        fs.set_option(k, {"grp_ranges": 1}.get(k, 0))
+    for a, b in zip(out[0], out[1]):
+        assert torch.equal(a.view(torch.int32), b.view(torch.int32))

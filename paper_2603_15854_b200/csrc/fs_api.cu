@@ -53,6 +53,9 @@ struct fs_ctx {
   int pair_min_bn = 32;            // auto: use the pair kernel from this MMA N upwards (measured)
   int topk_mode = 0;               // fused top-k: 0 auto, 1 candidate lists in the epilogue, 2 via raw logits
   int topk_spans = 1;
+  int* grp_rowcnt = nullptr;       // [256] per-row counters of the warp-per-group stage 2 (kept at 0)
+  void* gscratch = nullptr;        // [B][n_groups] group states of the warp-per-group stage 2
+  size_t gscratch_bytes = 0;
   int grp_ranges = 1;              // grouped stage 2: host-computed group slot ranges (0 = device binary search)              // raw-logit route: span maxima + gather (1) or full chunk selection (0)
   int* topk_rowcnt = nullptr;      // [256] per-row candidate counters of the list route (kept at 0 between calls)
   int fuse_reduce = 1;             // single-group sampling without log-mass: last CTA finalizes (no stage 2)
@@ -410,11 +413,30 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
     const int* grp_lo = nullptr;
     if (a.n_groups > 1 && ctx->grp_ranges && (st = group_ranges(ctx, lay, a.n_groups, &grp_lo)) != FS_OK)
       return st;
+    fs::State* gscratch = nullptr;
+    if (grp_lo) {                             // warp-per-(row, group) stage 2: scratch + row counters
+      if (!ctx->grp_rowcnt) {
+        e = cudaMalloc(&ctx->grp_rowcnt, 256 * sizeof(int));
+        if (e != cudaSuccess) return fail(FS_ERR_OOM, "group row counter cudaMalloc failed");
+        e = cudaMemset(ctx->grp_rowcnt, 0, 256 * sizeof(int));
+        if (e != cudaSuccess) return cuda_fail(e, "group row counter memset");
+      }
+      const size_t need = (size_t)Bc * a.n_groups * sizeof(fs::State);
+      if (need > ctx->gscratch_bytes) {
+        if (ctx->gscratch) cudaFree(ctx->gscratch);
+        ctx->gscratch = nullptr;
+        ctx->gscratch_bytes = 0;
+        e = cudaMalloc(&ctx->gscratch, need);
+        if (e != cudaSuccess) return fail(FS_ERR_OOM, "group scratch cudaMalloc failed");
+        ctx->gscratch_bytes = need;
+      }
+      gscratch = static_cast<fs::State*>(ctx->gscratch);
+    }
     e = fs::launch_reduce(part, part_group, lay, Bc, a.n_groups, a.idx_out ? a.idx_out + r0 : nullptr,
                           a.score_out ? a.score_out + r0 : nullptr, a.logZ_out ? a.logZ_out + r0 : nullptr,
                           a.groups_out ? a.groups_out + (size_t)r0 * a.n_groups : nullptr, stream,
                           ctx->pdl != 0 && !ctx->time_stage1, a.logprob_out ? a.logprob_out + r0 : nullptr,
-                          grp_lo);
+                          grp_lo, gscratch, grp_lo ? ctx->grp_rowcnt : nullptr);
     if (e != cudaSuccess) return cuda_fail(e, "stage-2 reduce launch");
   }
   return FS_OK;
@@ -640,6 +662,8 @@ void fs_ctx_destroy(fs_ctx* ctx) {
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->topk_rowcnt) cudaFree(ctx->topk_rowcnt);
   if (ctx->fin_buf) cudaFree(ctx->fin_buf);
+  if (ctx->grp_rowcnt) cudaFree(ctx->grp_rowcnt);
+  if (ctx->gscratch) cudaFree(ctx->gscratch);
   fs_comm_window_destroy(ctx);
   delete ctx;
 }

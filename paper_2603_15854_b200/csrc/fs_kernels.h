@@ -107,7 +107,9 @@ struct SlotLayout {
 cudaError_t launch_reduce(const State* part, const int* part_group, const SlotLayout& lay, int B, int n_groups,
                           int32_t* idx_out, float* score_out, float* logZ_out, fs_summary* groups_out,
                           cudaStream_t stream, bool pdl, float* logprob_out = nullptr,
-                          const int* grp_lo = nullptr);   // [n_groups+1] first slot per group (host-computed)
+                          const int* grp_lo = nullptr,    // [n_groups+1] first slot per group (host-computed)
+                          State* gscratch = nullptr,      // [B][n_groups] group states (warp-per-group kernel)
+                          int* row_ctr = nullptr);        // [B] zeroed counters (warp-per-group kernel)
 // Standalone sampler over materialised logits [B][ld] (bf16 or fp32): candidates per (V-block, row).
 cudaError_t launch_logits_sample(fs_dtype dtype, const void* logits, int64_t ld, const float* bias,
                                  const float* temperature, const uint32_t* mask, int64_t mask_words, int B, int V,

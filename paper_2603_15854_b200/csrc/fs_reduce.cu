@@ -122,6 +122,57 @@ reduce_groups_kernel(const State* __restrict__ part, const int* __restrict__ par
   }
 }
 
+// Grouped stage 2 with host-computed group slot ranges: one warp per (row, group) -- lane L merges
+// the group's slots L, L+32, ... then a fixed xor tree -> (M_k, I_k, L_k); the group state goes to
+// scratch and the last warp of the row (per-row counter, threadFence pattern) merges the row's
+// n_groups states in group order (deterministic) into idx / score / logZ / log-prob.
+__global__ void __launch_bounds__(256)
+reduce_groups_warp_kernel(const State* __restrict__ part, int B, int n_groups, const int* __restrict__ grp_lo,
+                          State* gstate, int* row_ctr, int32_t* idx_out, float* score_out, float* logZ_out,
+                          fs_summary* groups_out, float* logprob_out) {
+  sm100::pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int k = blockIdx.x * 8 + (threadIdx.x >> 5), b = blockIdx.y;
+  if (k >= n_groups) return;
+  const int lo = grp_lo[k], hi = grp_lo[k + 1];
+  State g = state_empty();
+#pragma unroll 4
+  for (int s = lo + lane; s < hi; s += 32) g = state_merge(g, part[(size_t)s * B + b]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const State other = shfl_xor_state(g, o);
+    g = (lane & o) ? state_merge(other, g) : state_merge(g, other);
+  }
+  int last = 0;
+  if (lane == 0) {
+    if (groups_out) groups_out[(size_t)b * n_groups + k] = to_summary(g);
+    gstate[(size_t)b * n_groups + k] = g;
+    __threadfence();
+    last = atomicAdd(&row_ctr[b], 1) == n_groups - 1;
+  }
+  last = __shfl_sync(0xFFFFFFFFu, last, 0);
+  if (!last) return;
+  __threadfence();
+  State acc = state_empty();
+  for (int kk = lane; kk < n_groups; kk += 32) {
+    const uint4 u = __ldcg(reinterpret_cast<const uint4*>(gstate + (size_t)b * n_groups + kk));
+    acc = state_merge(acc, State{u.x, (int32_t)u.y, __uint_as_float(u.z), u.w});
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const State other = shfl_xor_state(acc, o);
+    acc = (lane & o) ? state_merge(other, acc) : state_merge(acc, other);
+  }
+  if (lane == 0) {
+    const fs_summary f = to_summary(acc);
+    if (idx_out) idx_out[b] = f.idx;
+    if (score_out) score_out[b] = f.max_score;
+    if (logZ_out) logZ_out[b] = f.log_mass;
+    if (logprob_out) logprob_out[b] = logprob_of(acc);
+    row_ctr[b] = 0;                            // ready for the next call
+  }
+}
+
 __global__ void combine_kernel(const fs_summary* __restrict__ gathered, int n, int B, int32_t* idx_out,
                                float* score_out, float* logZ_out) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -159,7 +210,8 @@ __global__ void gumbel_kernel(const uint32_t* r, float* g, int64_t n) {
 
 cudaError_t launch_reduce(const State* part, const int* part_group, const SlotLayout& lay, int B, int n_groups,
                           int32_t* idx_out, float* score_out, float* logZ_out, fs_summary* groups_out,
-                          cudaStream_t stream, bool pdl, float* logprob_out, const int* grp_lo) {
+                          cudaStream_t stream, bool pdl, float* logprob_out, const int* grp_lo,
+                          State* gscratch, int* row_ctr) {
   cudaLaunchConfig_t cfg = {};
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -172,6 +224,12 @@ cudaError_t launch_reduce(const State* part, const int* part_group, const SlotLa
     cfg.blockDim = dim3(128);
     return cudaLaunchKernelEx(&cfg, reduce_rows_kernel, part, part_group, lay.n_slots, B, idx_out, score_out,
                               logZ_out, groups_out, logprob_out);
+  }
+  if (grp_lo && gscratch && row_ctr && B <= 64) {   // measured: B=32 14.1 -> 10.3 us; B=256 19.4 -> 24.0
+    cfg.gridDim = dim3((n_groups + 7) / 8, B);
+    cfg.blockDim = dim3(256);
+    return cudaLaunchKernelEx(&cfg, reduce_groups_warp_kernel, part, B, n_groups, grp_lo, gscratch, row_ctr,
+                              idx_out, score_out, logZ_out, groups_out, logprob_out);
   }
   cfg.gridDim = dim3(B);
   cfg.blockDim = dim3(kReduceThreads);

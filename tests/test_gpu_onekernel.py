@@ -242,7 +242,7 @@ def test_one_kernel_log_mass_and_shard_equal_stage2(B):
 
 @pytest.mark.parametrize("opts", [{}, {"pair": 0}, {"pair": 1}, {"max_ctas": 37}, {"unit_rows": 64},
                                   {"force_simt": 1}])
-@pytest.mark.parametrize("V,g,B", [(20011, 4096, 9), (9000, 128, 40), (5000, 640, 3)])
+@pytest.mark.parametrize("V,g,B", [(20011, 4096, 9), (9000, 128, 40), (5000, 640, 3), (7000, 1024, 100)])
 def test_grouped_host_slot_ranges_equal_device_search(opts, V, g, B):
     # grouped stage 2 with host-computed group slot ranges (warp per (row, group); the last warp of a
     # row merges the groups in order) == the block-per-row kernel with a device binary search over the

@@ -22,6 +22,23 @@ for pair in (0, 1):
     parts = [fs.sample_shard(h, W[a:b].contiguous(), a, 3000, seed=1, step=2).raw for a, b in ((0, 1500), (1500, 3000))]
     fs.combine_summaries(torch.stack(parts))
 fs.set_option("pair", -1)
+# one-kernel paths added later: logZ finalize in the last CTA (B <= 16), grouped warp-per-group stage 2,
+# in-kernel host staging, logits-sampler finalize, fused top-k span gather
+h8, tau8, mask8 = h[:8].contiguous(), tau[:8].contiguous(), mask[:8].contiguous()
+fs.sample(h8, W, bias=bias, temperature=tau8, mask=mask8, seed=1, step=2, return_logprob=True)
+fs.sample_shard(h8, W[1000:2000].contiguous(), 1000, 3000, seed=1, step=2)
+fs.sample_grouped(h, W, group_size=256, bias=bias, temperature=tau, mask=mask, seed=1, step=2)
+for pdl_w in (0, 1):
+    fs.set_option("pdl_w", pdl_w)
+    out = torch.empty(40, dtype=torch.int32).pin_memory()
+    for st in range(3):
+        fs.sample_from_host(h.cpu().pin_memory(), W, temperature_host=tau.cpu().pin_memory(), bias=bias, seed=1,
+                            step=st, h_dev=torch.empty_like(h), idx_host=out)
+fs.set_option("pdl_w", 0)
+fs.sample_logits(h.float() @ W.float().t(), bias=bias, temperature=tau, mask=mask, seed=1, step=3, return_score=True)
+fs.set_option("topk_mode", 2)
+fs.sample(h, W, temperature=tau, seed=1, step=2, top_k=30, top_p=0.9)
+fs.set_option("topk_mode", 0)
 fs.set_option("force_simt", 1)
 fs.sample(h, W, bias=bias, temperature=tau, mask=mask, seed=1, step=2)
 fs.set_option("force_simt", 0)

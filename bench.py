@@ -547,6 +547,7 @@ def run_tp(args):
     local_s = fs.Summaries.empty(B, device=dev)
     gathered = torch.empty(world, B, 3, dtype=torch.int32, device=dev)
     ctr = [0]
+    fs.set_option("pdl_w", 1)            # W of the next shard step streams before the dependency wait
 
     def step():
         ctr[0] += 1

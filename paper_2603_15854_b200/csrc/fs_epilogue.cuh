@@ -487,8 +487,14 @@ __device__ __forceinline__ void stage_h_slice(const void* h_host, const void* h_
   if (et == 0) atomicAdd(h_bar, 1u);
 }
 // Producer side: wait until every CTA staged its slice, then order the TMA reads after it.
+// Bounded: if the grid's CTAs cannot all be resident (a shared GPU), trap after ~10 s instead of
+// hanging -- the launch then fails with an error the caller sees.
 __device__ __forceinline__ void wait_h_staged(const unsigned int* h_bar) {
-  while (sm100::ld_acquire_gpu(h_bar) < gridDim.x) __nanosleep(64);
+  const uint64_t t0 = sm100::globaltimer();
+  while (sm100::ld_acquire_gpu(h_bar) < gridDim.x) {
+    __nanosleep(64);
+    if (sm100::globaltimer() - t0 > 10000000000ull) __trap();
+  }
   sm100::fence_proxy_async_global();
 }
 

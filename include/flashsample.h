@@ -90,7 +90,10 @@ void fs_ctx_destroy(fs_ctx* ctx);
  *       the stage-1 kernel: every CTA folds its candidate per row into a 64-bit atomicMax of
  *       (order key << 32 | ~idx) in the context's workspace, and the last CTA to finish writes
  *       idx_out / score_out (Alg. 2 stage 2, done in L2 instead of a second kernel).
- *       0 = separate stage-2 reduce kernel.  Same results bit for bit.
+ *       Also: fs_sample_logits (B <= 256, no log-mass) ends in its last block; single-group calls
+ *       with log-mass outputs (logZ / log-prob / a TP shard summary) with B <= 16 run the
+ *       stage-2 row reduce in the last stage-1 CTA.  0 = separate stage-2 reduce kernels.  Same
+ *       results bit for bit.
  *   "pdl_w" (default 0): launch stage 1 with programmatic dependent launch.  The kernel then starts
  *       while the preceding kernel on the stream finishes and streams its first W tiles BEFORE
  *       waiting for it; every other input (h, bias, temperature, mask, seeds, steps) is read and
@@ -100,7 +103,10 @@ void fs_ctx_destroy(fs_ctx* ctx);
  *   Tuning / testing: "force_simt" (1 = CUDA-core kernel), "max_ctas" (cap the persistent grid,
  *   0 = number of SMs), "pdl" (stage 1 -> stage 2 programmatic launch, default 1), "pair" (CTA-pair
  *   kernel: -1 auto, 0 off, 1 on), "stages", "kbps", "unit_rows", "l2promo", "w_policy",
- *   "topk_mode", "time_stage1" (below); "dbg_no_mma", "dbg_no_epi" (debug: results are garbage). */
+ *   "topk_mode", "topk_spans" (fused top-k raw-logit route: 1 span maxima + gather, 0 chunk
+ *   selection), "grp_ranges" (grouped stage 2: 1 host slot ranges, 0 device search), "time_stage1"
+ *   (below); debug: "dbg_no_mma", "dbg_no_epi" (results are garbage), "dbg_times" (device pointer
+ *   to [grid][8] u64 per-CTA timestamps, tools/exp_times.py; 0 = off). */
 fs_status fs_ctx_set_option(fs_ctx* ctx, const char* name, int64_t value);
 /* Measurement hook (used by bench.py for the roofline figure).  With option "time_stage1" = 1
  * every call records a CUDA event pair around each stage-1 (fused kernel) launch on the call's
@@ -114,8 +120,8 @@ fs_status fs_ctx_query(fs_ctx* ctx, const char* name, double* out);
  *   h [B,D], W [V,D] (dtype), bias/temperature/mask as above (mask_words = ceil(V/32)).
  *   idx_out   [B] int32 (required): sampled global vocabulary id, -1 for undefined rows.
  *   score_out [B] fp32 or NULL: the winning perturbed score max_v (l~_v + g_v).
- * Workload per call: W is streamed from HBM exactly once; only per-CTA candidates
- * (B x #CTA x 16 bytes) are written besides the outputs. */
+ * Workload per call: W is streamed from HBM exactly once; besides the outputs only B 64-bit
+ * atomics per CTA (one-kernel finalize) or per-CTA candidates (B x #CTA x 16 bytes) are written. */
 fs_status fs_sample(fs_ctx* ctx, fs_dtype dtype,
                     const void* h, const void* W,
                     const float* bias, const float* temperature, const uint32_t* mask,

@@ -61,12 +61,18 @@ __device__ __forceinline__ void prq_bits4(uint32_t vq, uint32_t k0, uint32_t k1,
                                           uint32_t (&rr)[4]) {
   const U4 o = philox4x32_10(vq, 0x80000000u, c2, c3, k0, k1);
   const int a = lane & 3;
+  // y = (o) rotated left by a (two predicated rotation stages, 8 SEL), so y[r] = o[(a + r) & 3];
+  // round r sends o[(a - r) & 3] = y[(4 - r) & 3]
+  const bool s1 = a & 1, s2 = a & 2;
+  uint32_t t0 = s1 ? o.y : o.x, t1 = s1 ? o.z : o.y, t2 = s1 ? o.w : o.z, t3 = s1 ? o.x : o.w;
+  const uint32_t y0 = s2 ? t2 : t0, y1 = s2 ? t3 : t1, y2 = s2 ? t0 : t2, y3 = s2 ? t1 : t3;
+  const uint32_t send[4] = {y0, y3, y2, y1};
   uint32_t got[4];
 #pragma unroll
-  for (int r = 0; r < 4; ++r)
-    got[r] = __shfl_sync(0xFFFFFFFFu, sel4(o.x, o.y, o.z, o.w, (a - r) & 3), (lane & ~3) | ((a + r) & 3));
-#pragma unroll
-  for (int c = 0; c < 4; ++c) rr[c] = sel4(got[0], got[1], got[2], got[3], (c - a) & 3);
+  for (int r = 0; r < 4; ++r) got[r] = __shfl_sync(0xFFFFFFFFu, send[r], (lane & ~3) | ((a + r) & 3));
+  // rr[c] = got[(c - a) & 3]: got rotated right by a
+  t0 = s1 ? got[3] : got[0]; t1 = s1 ? got[0] : got[1]; t2 = s1 ? got[1] : got[2]; t3 = s1 ? got[2] : got[3];
+  rr[0] = s2 ? t2 : t0; rr[1] = s2 ? t3 : t1; rr[2] = s2 ? t0 : t2; rr[3] = s2 ? t1 : t3;
 }
 
 // ---------------------------------------------------------------------------------------

@@ -55,7 +55,8 @@ typedef enum {
   FS_ERR_INVALID = 1,      /* bad argument (NULL required pointer, size < 1, misalignment, ...) */
   FS_ERR_UNSUPPORTED = 2,  /* valid but not supported by this build (e.g. no sm_100 device)    */
   FS_ERR_CUDA = 3,         /* a CUDA runtime / driver call failed (message in fs_last_error)   */
-  FS_ERR_OOM = 4           /* workspace allocation failed                                      */
+  FS_ERR_OOM = 4,          /* workspace allocation failed                                      */
+  FS_ERR_NCCL = 5          /* an NCCL call or the communicator failed (fs_comm_init / fs_sample_tp) */
 } fs_status;
 
 typedef enum { FS_BF16 = 0, FS_F32 = 1 } fs_dtype;
@@ -82,7 +83,9 @@ const char* fs_last_error(void);
  * Fails with FS_ERR_UNSUPPORTED if the device is not compute capability 10.0 (B200).
  * A context owns one workspace (candidate buffers, the finalize maxima / counter, top-k lists):
  * calls on one context must be ordered -- one stream at a time, or streams ordered by events.
- * Use one context per concurrently sampling stream. */
+ * Use one context per concurrently sampling stream (the Python binding keys contexts by
+ * (device, stream)).  Host-side context state is guarded by a lock, so concurrent calls from
+ * several host threads are safe as long as each uses its own context (or serialises its streams). */
 fs_status fs_ctx_create(int device, fs_ctx** out);
 void fs_ctx_destroy(fs_ctx* ctx);
 /* Options (name, value); unknown names -> FS_ERR_INVALID.
@@ -100,6 +103,8 @@ void fs_ctx_destroy(fs_ctx* ctx);
  *       every output written only after the wait.  Contract: W must not be written by the kernel
  *       immediately preceding the call on the same stream (LM-head weights are read-only while
  *       decoding).  Saves the launch gap and the pipeline fill of back-to-back decode steps.
+ *       1 = only for batch chunks of at most "pdl_w_max_b" rows (default 128: larger batches are
+ *       tensor/power-bound and two overlapping steps only share the power budget); 2 = always.
  *   Tuning / testing: "force_simt" (1 = CUDA-core kernel), "max_ctas" (cap the persistent grid,
  *   0 = number of SMs), "pdl" (stage 1 -> stage 2 programmatic launch, default 1), "pair" (CTA-pair
  *   kernel: -1 auto, 0 off, 1 on), "stages", "kbps", "unit_rows", "l2promo", "w_policy",
@@ -113,7 +118,11 @@ fs_status fs_ctx_set_option(fs_ctx* ctx, const char* name, int64_t value);
  * stream (PDL between stage 1 and stage 2 is disabled while timing).  fs_ctx_query(ctx,
  * "stage1_ms", &out) waits for the recorded events, returns the summed stage-1 milliseconds and
  * resets the record; "stage1_launches" returns the number of recorded launches (before a
- * "stage1_ms" query resets it).  Unknown names -> FS_ERR_INVALID. */
+ * "stage1_ms" query resets it).  Other queries: "num_sms"; "nccl_world" (fs_comm_init's world, 0 = no
+ * communicator); "comm_timeouts" (f2 exchange waits that
+ * gave up); "staging_timeouts" (fs_sample_staged grid barriers that gave up, see there);
+ * "staged_fallbacks" (fs_sample_staged calls staged by the copy kernel because the grid could not
+ * be co-resident).  Unknown names -> FS_ERR_INVALID. */
 fs_status fs_ctx_query(fs_ctx* ctx, const char* name, double* out);
 
 /* fs_sample -- fused LM-head projection + exact Gumbel-max sampling (Alg. 2).
@@ -134,10 +143,14 @@ fs_status fs_sample(fs_ctx* ctx, fs_dtype dtype,
  * option "fuse_reduce" on) the sampling kernel stages h itself: every CTA copies its slice of
  * h_host into h_dev over PCIe after the dependency wait, a grid-wide counter orders the slices
  * before the first h load, and W streaming starts meanwhile -- no copy kernel, no copy engine.
- * Otherwise fs_copy_async stages h before fs_sample.  The grid barrier needs all (#SMs)
- * persistent CTAs co-resident, which holds unless the GPU is shared (MPS / green contexts).
- * idx_out / score_out may also be pinned host memory (see fs_copy_async).  Results equal
- * fs_sample on the same h. */
+ * Otherwise fs_copy_async stages h before fs_sample.  The grid barrier needs all persistent CTAs
+ * co-resident: the call checks the occupancy of the exact kernel configuration (and "max_ctas"
+ * against the SM count) and stages with the copy kernel instead when the grid cannot fit
+ * (query "staged_fallbacks").  Should the CTAs still not be co-resident at run time (a GPU shared
+ * through MPS or green contexts), the barrier gives up after ~5 s: the call completes, every row
+ * is reported undefined (idx -1, score -inf) and "staging_timeouts" counts it -- no trap, no
+ * sticky CUDA error.  idx_out / score_out may also be pinned host memory (see fs_copy_async).
+ * Results equal fs_sample on the same h. */
 fs_status fs_sample_staged(fs_ctx* ctx, fs_dtype dtype, const void* h_host, void* h_dev, const void* W,
                            const float* bias, const float* temperature, const uint32_t* mask, uint64_t seed,
                            uint64_t step, int B, int D, int V, int32_t* idx_out, float* score_out, void* stream);
@@ -259,10 +272,13 @@ fs_status fs_combine_summaries(const fs_summary* gathered, int n, int B,
  * fs_comm_window_open: map the peers' windows from the gathered handles [world] (entry `rank`
  *   is ignored).  Peers may be other GPUs (peer access over NVLink) or the same GPU.
  * fs_sample_tp_push: fs_sample_shard + push + wait + fs_combine_summaries in stream order;
- *   every rank gets the identical idx_out (score_out, logZ_out optional).  All ranks must call it
- *   the same number of times (the step epoch is a per-context counter).  A peer that does not
- *   arrive within ~10 s makes the wait give up: idx_out = -1 and fs_ctx_query("comm_timeouts")
- *   counts it.
+ *   every rank gets the identical idx_out (score_out, logZ_out optional).  For B <= 256 the push is
+ *   fused into the shard sampler's last reduction step (the finalizing stage-1 CTA for B <= 16,
+ *   else the stage-2 row reduce): it stores the records into every peer window and releases the
+ *   flags itself, and one PDL-chained single-block kernel waits for the n flags and combines.
+ *   Larger B push from a separate kernel.  All ranks must call it the same number of times (the
+ *   step epoch is a per-context counter).  A peer that does not arrive within ~10 s makes the wait
+ *   give up: idx_out = -1 and fs_ctx_query("comm_timeouts") counts it.
  * fs_comm_window_destroy: unmap the peers and free the window. */
 typedef struct { unsigned char bytes[64]; } fs_ipc_handle;
 fs_status fs_comm_window_create(fs_ctx* ctx, int world, int rank, int B_max, fs_ipc_handle* handle_out);
@@ -273,6 +289,32 @@ fs_status fs_sample_tp_push(fs_ctx* ctx, fs_dtype dtype, const void* h, const vo
                             int64_t vocab_offset, int64_t V_total,
                             int32_t* idx_out, float* score_out, float* logZ_out, void* stream);
 fs_status fs_comm_window_destroy(fs_ctx* ctx);
+
+/* ---- NCCL-backed vocabulary-sharded sampling (§4.2; Alg. A.4) ----------------
+ * The NCCL form of the exchange: Alg. A.4 line 4 "all-gather the per-shard summaries".
+ * The library resolves NCCL at run time from the process (torch.distributed's libnccl.so.2) or
+ * $FS_NCCL_LIB; without NCCL these calls return FS_ERR_UNSUPPORTED and nothing else is affected.
+ * fs_comm_unique_id: write a fresh ncclUniqueId (128 opaque bytes) to id_out -- on ONE rank; the
+ *   caller broadcasts it to the others by any host transport (e.g. torch.distributed).
+ * fs_comm_init: create this context's NCCL communicator (collective over the `world` ranks, each
+ *   with its own context on its own GPU; blocks until all ranks joined).  Replaces a previous one.
+ * fs_sample_tp: one sharded decode step on the caller's stream, all inside the library:
+ *   fs_sample_shard(W_shard) -> this rank's [B] summaries (M, I, L)
+ *   -> ncclAllGather of the B x 12-byte records into [world][B] (context workspace)
+ *   -> outer selection (fs_combine_summaries): idx_out [B] identical on every rank, equal to
+ *      fs_sample on the unsharded W (global ids; reading R8 max reuse), score_out / logZ_out
+ *      optional, per_rank_out [world][B] fs_summary (device) or NULL: the gathered records.
+ *   Arguments as fs_sample_shard.  Asynchronous; FS_ERR_NCCL when the collective cannot be
+ *   enqueued or the communicator reports an asynchronous error (ncclCommGetAsyncError, checked
+ *   at every call).
+ * fs_comm_destroy: release the communicator (also done by fs_ctx_destroy). */
+fs_status fs_comm_unique_id(void* id_out);
+fs_status fs_comm_init(fs_ctx* ctx, const void* nccl_unique_id, int world, int rank);
+fs_status fs_sample_tp(fs_ctx* ctx, fs_dtype dtype, const void* h, const void* W_shard, const float* bias_shard,
+                       const float* temperature, const uint32_t* mask, uint64_t seed, uint64_t step, int B, int D,
+                       int V_local, int64_t vocab_offset, int64_t V_total, int32_t* idx_out, float* score_out,
+                       float* logZ_out, fs_summary* per_rank_out, void* stream);
+fs_status fs_comm_destroy(fs_ctx* ctx);
 
 /* fs_merge_summaries -- online binary merge of two summaries of disjoint vocabulary sets
  * (Alg. A.3, Lemma "binary merge" P:315-349, realised by max reuse):
@@ -286,9 +328,10 @@ fs_status fs_merge_summaries(const fs_summary* a, const fs_summary* b, fs_summar
  * host -> device copy of h [, temperature, mask]).  A kernel on `stream` copies `bytes` from
  * `src` (pinned host memory, read over PCIe through its unified address, or device memory) to
  * device memory `dst`; both 16-byte aligned.  With option "pdl_w" it is launched with
- * programmatic dependent launch: it loads src before and stores dst only after the preceding
- * kernel on the stream completes (that kernel may still be reading dst), and the next fs_sample
- * may start streaming W while the copy runs.  Asynchronous; the caller keeps src alive and
+ * programmatic dependent launch: it stores dst only after the preceding kernel on the stream
+ * completes (that kernel may still be reading dst) and loads a pinned-host src before that wait
+ * (a device src, which the preceding kernel may have produced, only after it); the next
+ * fs_sample may start streaming W while the copy runs.  Asynchronous; the caller keeps src alive and
  * unchanged until the stream passes the copy.  FS_ERR_INVALID: NULL / misaligned pointers or a
  * pageable (unregistered) host src.
  * fs_sample writes idx_out / score_out with plain stores, so they may also point to pinned host

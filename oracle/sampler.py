@@ -145,6 +145,7 @@ class TopKResult:
     kept: list                # per row: global ids of the kept set (top-k, then top-p), sorted
     kth_margin: np.ndarray    # [R] l~ gap at the top-k boundary (rank k vs k+1; inf if none)
     p_margin: np.ndarray      # [R] |cumsum before the top-p cut - p| (decision margin)
+    near: list = None         # per row: kept ids with s >= s1 - NEAR_TIE (the north-star near-tie set)
 
 
 def topk_topp_sample(sc: Scores, top_k: int, top_p: float = 1.0) -> TopKResult:
@@ -160,6 +161,7 @@ def topk_topp_sample(sc: Scores, top_k: int, top_p: float = 1.0) -> TopKResult:
     kth = np.full(R, np.inf)
     pm = np.full(R, np.inf)
     kept_all = []
+    near_all = []
     for r in range(R):
         lt = sc.ltilde[r]
         order = np.lexsort((sc.v_global, -lt))               # l~ desc, id asc
@@ -170,6 +172,7 @@ def topk_topp_sample(sc: Scores, top_k: int, top_p: float = 1.0) -> TopKResult:
         cand = cand[np.isfinite(lt[cand])]
         if cand.size == 0:
             kept_all.append([])
+            near_all.append([])
             continue
         q = np.exp(lt[cand] - lt[cand[0]])
         q = q / q.sum()
@@ -189,7 +192,8 @@ def topk_topp_sample(sc: Scores, top_k: int, top_p: float = 1.0) -> TopKResult:
         rest = s[keep != j]
         gap[r] = best - rest.max() if rest.size else np.inf
         kept_all.append(sorted(int(sc.v_global[x]) for x in keep))
-    return TopKResult(idx=idx, s1=s1, gap=gap, kept=kept_all, kth_margin=kth, p_margin=pm)
+        near_all.append(sorted(int(sc.v_global[x]) for x, sx in zip(keep, s) if sx >= best - NEAR_TIE))
+    return TopKResult(idx=idx, s1=s1, gap=gap, kept=kept_all, kth_margin=kth, p_margin=pm, near=near_all)
 
 
 def log_prob(sc: Scores, res: "FlatResult") -> np.ndarray:

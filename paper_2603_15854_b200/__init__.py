@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes
 import dataclasses
+import threading
 
 import torch
 
@@ -23,33 +24,58 @@ from ._lib import FS_BF16, FS_F32, FlashSampleError
 __all__ = ["sample", "sample_grouped", "sample_logits", "sample_shard", "combine_summaries", "merge_summaries",
            "random_bits", "gumbel_from_bits", "Summaries", "context", "set_option", "query",
            "FlashSampleError", "version", "sample_from_host", "comm_window_create", "comm_window_open",
-           "comm_window_destroy", "sample_tp_push"]
+           "comm_window_destroy", "sample_tp_push", "comm_unique_id", "comm_init", "comm_destroy", "sample_tp"]
 
-_ctx = {}
+_ctx = {}            # (device, CUDA stream handle) -> fs_ctx handle
+_opts = {}           # device -> {option: value}, applied to every context of that device
+_ctx_lock = threading.Lock()
 
 
 def version() -> str:
     return _lib.lib().fs_version().decode()
 
 
-def context(device: int | torch.device | None = None) -> int:
-    """The library context (ctypes handle) for a CUDA device, created on first use."""
+def _device_index(device) -> int:
     if device is None:
-        device = torch.cuda.current_device()
+        return torch.cuda.current_device()
     if isinstance(device, torch.device):
-        device = device.index if device.index is not None else torch.cuda.current_device()
-    if device not in _ctx:
-        h = ctypes.c_void_p()
-        _lib.check(_lib.lib().fs_ctx_create(int(device), ctypes.byref(h)), "fs_ctx_create")
-        _ctx[device] = h
-    return _ctx[device]
+        return device.index if device.index is not None else torch.cuda.current_device()
+    return int(device)
+
+
+def context(device: int | torch.device | None = None, stream=None) -> ctypes.c_void_p:
+    """The library context (ctypes handle) for (device, stream), created on first use.
+    A context owns one device workspace, so calls on it must be stream-ordered
+    (include/flashsample.h): keying contexts by stream lets several streams -- or host threads
+    on their own streams -- sample concurrently.  `stream` defaults to the device's current
+    stream.  Options set through set_option() apply to every context of the device."""
+    dev = _device_index(device)
+    if stream is None:
+        stream = torch.cuda.current_stream(dev)
+    key = (dev, int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream))
+    with _ctx_lock:
+        if key not in _ctx:
+            h = ctypes.c_void_p()
+            _lib.check(_lib.lib().fs_ctx_create(dev, ctypes.byref(h)), "fs_ctx_create")
+            for name, value in _opts.get(dev, {}).items():
+                _lib.check(_lib.lib().fs_ctx_set_option(h, name.encode(), int(value)), "fs_ctx_set_option")
+            _ctx[key] = h
+        return _ctx[key]
 
 
 def set_option(name: str, value: int, device=None) -> None:
-    _lib.check(_lib.lib().fs_ctx_set_option(context(device), name.encode(), int(value)), "fs_ctx_set_option")
+    """Set a library option (fs_ctx_set_option) on every context of the device, present and future."""
+    dev = _device_index(device)
+    context(dev)                         # make sure the current stream's context exists
+    with _ctx_lock:
+        _opts.setdefault(dev, {})[name] = int(value)
+        handles = [h for (d, _), h in _ctx.items() if d == dev]
+    for h in handles:
+        _lib.check(_lib.lib().fs_ctx_set_option(h, name.encode(), int(value)), "fs_ctx_set_option")
 
 
 def query(name: str, device=None) -> float:
+    """fs_ctx_query on the context of the device's current stream."""
     out = ctypes.c_double()
     _lib.check(_lib.lib().fs_ctx_query(context(device), name.encode(), ctypes.byref(out)), "fs_ctx_query")
     return out.value
@@ -164,6 +190,47 @@ def sample_tp_push(h, W_shard, vocab_offset: int, V_total: int, *, bias_shard=No
         _ptr(mask), seed & (2**64 - 1), step & (2**64 - 1), B, D, V_local, int(vocab_offset), int(V_total),
         _ptr(idx), _ptr(score), _ptr(logZ), _stream(h)), "fs_sample_tp_push")
     return (idx, score, logZ) if return_all else idx
+
+
+def comm_unique_id() -> bytes:
+    """A fresh NCCL unique id (128 bytes) for fs_comm_init; create it on one rank and broadcast it."""
+    buf = ctypes.create_string_buffer(128)
+    _lib.check(_lib.lib().fs_comm_unique_id(buf), "fs_comm_unique_id")
+    return buf.raw
+
+
+def comm_init(unique_id: bytes, world: int, rank: int, device=None) -> None:
+    """Create the library's NCCL communicator on this rank's context (collective; fs_comm_init)."""
+    if len(unique_id) != 128:
+        raise ValueError("unique_id must be the 128 bytes of comm_unique_id()")
+    buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+    _lib.check(_lib.lib().fs_comm_init(context(device), buf, int(world), int(rank)), "fs_comm_init")
+
+
+def comm_destroy(device=None) -> None:
+    _lib.check(_lib.lib().fs_comm_destroy(context(device)), "fs_comm_destroy")
+
+
+def sample_tp(h, W_shard, vocab_offset: int, V_total: int, *, bias_shard=None, temperature=None, mask=None,
+              seed: int = 0, step: int = 0, return_all: bool = False, per_rank: bool = False, out=None):
+    """One vocabulary-sharded step through the library's NCCL path (fs_sample_tp): shard summaries,
+    ncclAllGather of B x 12 bytes, outer selection.  idx [B] identical on every rank.
+    Returns idx, or (idx, score, logZ[, per-rank Summaries [world, B]]) with return_all."""
+    B, D, V_local = _check_inputs(h, W_shard, bias_shard, temperature, mask, V_total=V_total)
+    idx = out if out is not None else torch.empty(B, dtype=torch.int32, device=h.device)
+    score = torch.empty(B, dtype=torch.float32, device=h.device) if return_all else None
+    logZ = torch.empty(B, dtype=torch.float32, device=h.device) if return_all else None
+    ranks = None
+    if per_rank:
+        ranks = Summaries.empty(int(query("nccl_world", h.device)), B, device=h.device)
+    _lib.check(_lib.lib().fs_sample_tp(
+        context(h.device), _dtype_code(h, W_shard), _ptr(h), _ptr(W_shard), _ptr(bias_shard), _ptr(temperature),
+        _ptr(mask), seed & (2**64 - 1), step & (2**64 - 1), B, D, V_local, int(vocab_offset), int(V_total),
+        _ptr(idx), _ptr(score), _ptr(logZ), _ptr(ranks.raw) if ranks is not None else None, _stream(h)),
+        "fs_sample_tp")
+    if not return_all:
+        return idx
+    return (idx, score, logZ) + ((ranks,) if per_rank else ())
 
 
 @dataclasses.dataclass

@@ -18,10 +18,10 @@ EXPORTS = [
     "fs_sample_logits_ex", "fs_sample_shard",
     "fs_combine_summaries", "fs_merge_summaries", "fs_random_bits", "fs_gumbel_from_bits",
     "fs_comm_window_create", "fs_comm_window_open", "fs_sample_tp_push", "fs_comm_window_destroy",
-    "fs_copy_async", "fs_sample_staged",
+    "fs_copy_async", "fs_sample_staged", "fs_comm_unique_id", "fs_comm_init", "fs_sample_tp", "fs_comm_destroy",
 ]
 
-FS_OK, FS_ERR_INVALID, FS_ERR_UNSUPPORTED, FS_ERR_CUDA, FS_ERR_OOM = range(5)
+FS_OK, FS_ERR_INVALID, FS_ERR_UNSUPPORTED, FS_ERR_CUDA, FS_ERR_OOM, FS_ERR_NCCL = range(6)
 
 
 class SampleArgs(ctypes.Structure):
@@ -84,6 +84,10 @@ def lib() -> ctypes.CDLL:
     L.fs_comm_window_open.argtypes = [vp, ctypes.POINTER(IpcHandle)]
     L.fs_comm_window_destroy.argtypes = [vp]
     L.fs_sample_tp_push.argtypes = [vp, i32, vp, vp, vp, vp, vp, u64, u64, i32, i32, i32, i64, i64, vp, vp, vp, vp]
+    L.fs_comm_unique_id.argtypes = [vp]
+    L.fs_comm_init.argtypes = [vp, vp, i32, i32]
+    L.fs_comm_destroy.argtypes = [vp]
+    L.fs_sample_tp.argtypes = [vp, i32, vp, vp, vp, vp, vp, u64, u64, i32, i32, i32, i64, i64, vp, vp, vp, vp, vp]
     for name in EXPORTS:
         if name not in ("fs_version", "fs_status_str", "fs_last_error", "fs_ctx_destroy"):
             getattr(L, name).restype = i32

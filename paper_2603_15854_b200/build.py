@@ -13,11 +13,31 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libflashsample.so")
 SOURCES = ["fs_api.cu", "fs_fused_tc.cu", "fs_fused_tc2.cu", "fs_fused_simt.cu", "fs_reduce.cu", "fs_logits.cu", "fs_topk.cu"]
-HEADERS = ["fs_device.cuh", "fs_sm100.cuh", "fs_epilogue.cuh", "fs_kernels.h"]
+HEADERS = ["fs_device.cuh", "fs_sm100.cuh", "fs_epilogue.cuh", "fs_kernels.h", "fs_peer.cuh", "fs_nccl.h",
+           "fs_topk_epi.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nccl_flags() -> list:
+    """nccl.h of the pip NCCL torch loads (types only) and that library's path as the run-time
+    default (csrc/fs_nccl.h resolves NCCL with dlopen; nothing is linked)."""
+    try:
+        import nvidia.nccl
+        d = list(nvidia.nccl.__path__)[0]
+        if os.path.exists(os.path.join(d, "include", "nccl.h")):
+            flags = ["-I", os.path.join(d, "include")]
+            lib = os.path.join(d, "lib", "libnccl.so.2")
+            if os.path.exists(lib):
+                flags.append(f'-DFS_NCCL_DEFAULT_PATH="{lib}"')
+            return flags
+    except Exception:
+        pass
+    return ["-I", "/usr/include"]
+
+
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-         "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]
+         "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"), *_nccl_flags()]
 
 
 def _stale() -> bool:
@@ -48,7 +68,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose:
             sys.stdout.write(open(logf).read())
     tmp = LIB + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs]
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-ldl"]
     subprocess.check_call(cmd)
     os.replace(tmp, LIB)
     return LIB

@@ -4,14 +4,17 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/flashsample.h"
 #include "fs_device.cuh"
 #include "fs_kernels.h"
+#include "fs_nccl.h"
 
 #define FS_VERSION_STRING "flashsample-b200 0.1.0 (sm_100a)"
 
@@ -34,6 +37,10 @@ typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_
 }  // namespace
 
 struct fs_ctx {
+  // Host-side state (workspace pointers, descriptor / layout caches, counters) is guarded by this
+  // lock, so concurrent calls from several host threads cannot corrupt it.  The device workspace
+  // itself is still one per context: calls on one context must be stream-ordered (header).
+  std::recursive_mutex mu;
   int device = 0;
   int num_sms = 0;
   void* ws = nullptr;
@@ -60,8 +67,14 @@ struct fs_ctx {
   int* topk_rowcnt = nullptr;      // [256] per-row candidate counters of the list route (kept at 0 between calls)
   int fuse_reduce = 1;             // single-group sampling without log-mass: last CTA finalizes (no stage 2)
   int pdl_w = 0;                   // stage 1 launched with PDL, W streamed before the dependency wait
+                                   // (1: for batch chunks <= pdl_w_max_b rows, 2: always)
+  int pdl_w_max_b = 128;
   unsigned long long* dbg_times = nullptr;   // debug: per-CTA timeline of the fused kernels (tools/exp_times.py)
-  unsigned long long* fin_buf = nullptr;   // [256] row maxima + [1] CTA counter, 0 between calls
+  unsigned long long* fin_buf = nullptr;   // [256] row maxima + CTA counter + staging words (ensure_fin)
+  uint64_t staged_fallbacks = 0;           // fs_sample_staged calls staged by the copy kernel instead
+  int staging_check = 1;                   // testing: 0 skips the co-residency check of in-kernel staging
+  struct ResKey { int pair, bn, stages, kbps, xform, grid; };
+  std::vector<std::pair<ResKey, int>> res_cache;   // co-resident CTAs of a stage-1 configuration
   // f2 peer-memory exchange (fs_comm_window_*)
   char* comm_win = nullptr;        // this rank's window (cudaMalloc, exported by IPC)
   size_t comm_off_flags = 0, comm_off_acks = 0, comm_off_status = 0;
@@ -70,6 +83,12 @@ struct fs_ctx {
   bool comm_open = false;
   fs_summary* comm_local = nullptr;   // [B_max] this rank's shard summaries
   uint64_t comm_epoch = 0;
+  fs::PeerTab* comm_peertab = nullptr;  // device copy of the peers' window addresses (fused push)
+  // NCCL communicator of fs_comm_init / fs_sample_tp
+  ncclComm_t nccl = nullptr;
+  int nccl_world = 0, nccl_rank = 0;
+  fs_summary* tp_buf = nullptr;       // [1 + world][tp_bmax]: local summaries, then the gathered ones
+  int tp_bmax = 0;
   // tensor-map cache: encoding costs host microseconds per map; W maps are reused across calls
   struct MapKey { const void* base; int64_t inner, rows; int box, promo; };
   struct MapEnt { MapKey k; CUtensorMap m; };
@@ -158,13 +177,15 @@ fs_status group_ranges(fs_ctx* ctx, const fs::SlotLayout& L, int n_groups, const
   return FS_OK;
 }
 
-// One-kernel finalize buffer: [256] row maxima, CTA counter, staging barrier; zeroed once, left
-// zeroed by every call.
+// One-kernel finalize buffer: [256] row maxima, [256] CTA counter, [257] staging barrier (u32) +
+// staging-timeout flag (u32), [258] staging-timeout count; zeroed once, left zeroed by every call
+// (except the count).
+constexpr int kFinWords = 260;
 fs_status ensure_fin(fs_ctx* ctx) {
   if (ctx->fin_buf) return FS_OK;
-  cudaError_t e = cudaMalloc(&ctx->fin_buf, 258 * sizeof(unsigned long long));
+  cudaError_t e = cudaMalloc(&ctx->fin_buf, kFinWords * sizeof(unsigned long long));
   if (e != cudaSuccess) return fail(FS_ERR_OOM, "finalize buffer cudaMalloc failed");
-  e = cudaMemset(ctx->fin_buf, 0, 258 * sizeof(unsigned long long));
+  e = cudaMemset(ctx->fin_buf, 0, kFinWords * sizeof(unsigned long long));
   if (e != cudaSuccess) return cuda_fail(e, "finalize buffer memset");
   return FS_OK;
 }
@@ -271,6 +292,7 @@ struct PathArgs {
   const uint64_t* seeds = nullptr;
   const uint64_t* steps = nullptr;
   const void* h_host = nullptr;   // fs_sample_staged: pinned host h, staged into h by the kernel
+  const fs::PushCtx* push = nullptr;   // f2: the shard's summaries also go to the peer windows (B <= 256)
 };
 
 // time_stage1 option: record a start event now and return the end event to record after stage 1.
@@ -354,6 +376,7 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
     p.unit_rows = unit;
     p.part = part;
     p.part_group = part_group;
+    if (a.push) p.push = *a.push;
     cudaEvent_t ev_end = nullptr;
     if ((st = stage1_event(ctx, stream, &ev_end)) != FS_OK) return st;
     if (tc) {
@@ -377,15 +400,38 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
       CUtensorMap hmap;
       if ((st = make_map(ctx, &hmap, p.h, a.D, Bc, pair ? BN / 2 : BN)) != FS_OK) return st;
       p.wmaps = wmaps;
-      p.pdl_w = ctx->pdl_w && ctx->pdl && !ctx->time_stage1;
+      // PDL across steps: worth it while the step is bandwidth-bound; once it is tensor/power-bound
+      // (B > pdl_w_max_b, measured: B=256 loops ran 3-15% slower than isolated calls) the overlap of
+      // two steps' W streams only competes for the power budget
+      p.pdl_w = (ctx->pdl_w >= 2 || (ctx->pdl_w == 1 && Bc <= ctx->pdl_w_max_b)) && ctx->pdl && !ctx->time_stage1;
       if (fin) {
         p.fin_best = ctx->fin_buf;
         p.fin_ctr = reinterpret_cast<unsigned int*>(ctx->fin_buf + 256);
         p.idx_out = a.idx_out + r0;
         p.score_out = a.score_out ? a.score_out + r0 : nullptr;
         if (a.h_host) {
-          p.h_host = static_cast<const char*>(a.h_host) + (size_t)r0 * a.D * esz;
-          p.h_bar = reinterpret_cast<unsigned int*>(ctx->fin_buf + 257);
+          const void* hsrc = static_cast<const char*>(a.h_host) + (size_t)r0 * a.D * esz;
+          // the staging grid barrier needs every CTA resident at once: check the occupancy of the
+          // exact kernel; otherwise stage with the copy kernel (same results, one more launch)
+          const int xform = (p.bias || p.temperature || p.mask) ? 1 : 0;
+          const fs_ctx::ResKey rk{pair ? 1 : 0, BN, p.stages, p.kbps, xform, G};
+          int resident = -1;
+          for (const auto& r : ctx->res_cache)
+            if (!std::memcmp(&r.first, &rk, sizeof(rk))) resident = r.second;
+          if (resident < 0) {
+            e = pair ? fs::fused_tc2_resident(p, BN, a.lse, G, &resident) : fs::fused_tc_resident(p, BN, a.lse, &resident);
+            if (e != cudaSuccess) return cuda_fail(e, "occupancy query");
+            if (ctx->res_cache.size() >= 32) ctx->res_cache.erase(ctx->res_cache.begin());
+            ctx->res_cache.emplace_back(rk, resident);
+          }
+          if (G <= resident || !ctx->staging_check) {
+            p.h_host = hsrc;
+            p.h_bar = reinterpret_cast<unsigned int*>(ctx->fin_buf + 257);
+          } else {
+            e = fs::launch_copy_in(const_cast<void*>(p.h), hsrc, (size_t)Bc * a.D * esz, p.pdl_w, true, stream);
+            if (e != cudaSuccess) return cuda_fail(e, "staging copy kernel launch");
+            ++ctx->staged_fallbacks;
+          }
         }
       }
       if (fin_lse) {
@@ -436,7 +482,7 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
                           a.score_out ? a.score_out + r0 : nullptr, a.logZ_out ? a.logZ_out + r0 : nullptr,
                           a.groups_out ? a.groups_out + (size_t)r0 * a.n_groups : nullptr, stream,
                           ctx->pdl != 0 && !ctx->time_stage1, a.logprob_out ? a.logprob_out + r0 : nullptr,
-                          grp_lo, gscratch, grp_lo ? ctx->grp_rowcnt : nullptr);
+                          grp_lo, gscratch, grp_lo ? ctx->grp_rowcnt : nullptr, a.push);
     if (e != cudaSuccess) return cuda_fail(e, "stage-2 reduce launch");
   }
   return FS_OK;
@@ -595,6 +641,8 @@ fs_status run_topk_path(fs_ctx* ctx, const PathArgs& a, int k, float top_p, cuda
   return FS_OK;
 }
 
+#define FS_LOCK(ctx) std::lock_guard<std::recursive_mutex> fs_guard_((ctx)->mu)
+
 fs_status check_common(fs_ctx* ctx, fs_dtype dtype, const void* h, const void* W, int B, int D, int V) {
   if (!ctx) return fail(FS_ERR_INVALID, "ctx is NULL");
   if (dtype != FS_BF16 && dtype != FS_F32) return fail(FS_ERR_INVALID, "unknown dtype");
@@ -619,6 +667,7 @@ const char* fs_status_str(fs_status s) {
     case FS_ERR_UNSUPPORTED: return "FS_ERR_UNSUPPORTED";
     case FS_ERR_CUDA: return "FS_ERR_CUDA";
     case FS_ERR_OOM: return "FS_ERR_OOM";
+    case FS_ERR_NCCL: return "FS_ERR_NCCL";
   }
   return "FS_ERR_UNKNOWN";
 }
@@ -665,11 +714,13 @@ void fs_ctx_destroy(fs_ctx* ctx) {
   if (ctx->grp_rowcnt) cudaFree(ctx->grp_rowcnt);
   if (ctx->gscratch) cudaFree(ctx->gscratch);
   fs_comm_window_destroy(ctx);
+  fs_comm_destroy(ctx);
   delete ctx;
 }
 
 fs_status fs_ctx_set_option(fs_ctx* ctx, const char* name, int64_t value) {
   if (!ctx || !name) return fail(FS_ERR_INVALID, "ctx and name are required");
+  FS_LOCK(ctx);
   if (!strcmp(name, "force_simt")) ctx->force_simt = (int)value;
   else if (!strcmp(name, "max_ctas")) ctx->max_ctas = (int)value;
   else if (!strcmp(name, "pdl")) ctx->pdl = (int)value;
@@ -685,6 +736,8 @@ fs_status fs_ctx_set_option(fs_ctx* ctx, const char* name, int64_t value) {
   else if (!strcmp(name, "topk_spans")) ctx->topk_spans = (int)value;
   else if (!strcmp(name, "grp_ranges")) ctx->grp_ranges = (int)value;
   else if (!strcmp(name, "pdl_w")) ctx->pdl_w = (int)value;
+  else if (!strcmp(name, "pdl_w_max_b")) ctx->pdl_w_max_b = (int)value;
+  else if (!strcmp(name, "staging_check")) ctx->staging_check = (int)value;
   else if (!strcmp(name, "dbg_times")) ctx->dbg_times = reinterpret_cast<unsigned long long*>(value);
   else if (!strcmp(name, "pair_min_bn")) ctx->pair_min_bn = (int)value;
   else if (!strcmp(name, "topk_mode")) {
@@ -703,6 +756,7 @@ fs_status fs_ctx_set_option(fs_ctx* ctx, const char* name, int64_t value) {
 
 fs_status fs_ctx_query(fs_ctx* ctx, const char* name, double* out) {
   if (!ctx || !name || !out) return fail(FS_ERR_INVALID, "ctx, name and out are required");
+  FS_LOCK(ctx);
   if (!strcmp(name, "stage1_launches")) {
     *out = (double)ctx->ev_used;
     return FS_OK;
@@ -730,6 +784,23 @@ fs_status fs_ctx_query(fs_ctx* ctx, const char* name, double* out) {
     *out = (double)t;
     return FS_OK;
   }
+  if (!strcmp(name, "staging_timeouts")) {
+    unsigned t = 0;
+    if (ctx->fin_buf) {
+      cudaError_t e = cudaMemcpy(&t, reinterpret_cast<unsigned*>(ctx->fin_buf + 258), sizeof(t), cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) return cuda_fail(e, "staging status read");
+    }
+    *out = (double)t;
+    return FS_OK;
+  }
+  if (!strcmp(name, "nccl_world")) {
+    *out = ctx->nccl ? (double)ctx->nccl_world : 0.0;
+    return FS_OK;
+  }
+  if (!strcmp(name, "staged_fallbacks")) {
+    *out = (double)ctx->staged_fallbacks;
+    return FS_OK;
+  }
   if (!strcmp(name, "num_sms")) {
     *out = (double)ctx->num_sms;
     return FS_OK;
@@ -742,6 +813,7 @@ fs_status fs_sample(fs_ctx* ctx, fs_dtype dtype, const void* h, const void* W, c
                     int32_t* idx_out, float* score_out, void* stream) {
   fs_status s = check_common(ctx, dtype, h, W, B, D, V);
   if (s != FS_OK) return s;
+  FS_LOCK(ctx);
   if (!idx_out) return fail(FS_ERR_INVALID, "idx_out is required");
   PathArgs a{dtype, h, W, bias, temperature, mask, ((int64_t)V + 31) / 32, seed, step, B, D, V, 0,
              ((V + 127) / 128) * 128, false, idx_out, score_out, nullptr, nullptr, 1, nullptr};
@@ -753,6 +825,7 @@ fs_status fs_sample_staged(fs_ctx* ctx, fs_dtype dtype, const void* h_host, void
                            uint64_t step, int B, int D, int V, int32_t* idx_out, float* score_out, void* stream) {
   fs_status s = check_common(ctx, dtype, h_dev, W, B, D, V);
   if (s != FS_OK) return s;
+  FS_LOCK(ctx);
   if (!idx_out || !h_host) return fail(FS_ERR_INVALID, "h_host and idx_out are required");
   const size_t esz = dtype == FS_BF16 ? 2 : 4;
   cudaPointerAttributes at{};
@@ -779,6 +852,7 @@ fs_status fs_sample_grouped(fs_ctx* ctx, fs_dtype dtype, const void* h, const vo
                             float* logprob_out, fs_summary* groups_out, void* stream) {
   fs_status s = check_common(ctx, dtype, h, W, B, D, V);
   if (s != FS_OK) return s;
+  FS_LOCK(ctx);
   if (!idx_out) return fail(FS_ERR_INVALID, "idx_out is required");
   if (group_size < 128 || group_size % 128 != 0) return fail(FS_ERR_INVALID, "group_size must be a positive multiple of 128");
   const int n_groups = (V + group_size - 1) / group_size;
@@ -792,6 +866,7 @@ fs_status fs_sample_shard(fs_ctx* ctx, fs_dtype dtype, const void* h, const void
                           int V_local, int64_t vocab_offset, int64_t V_total, fs_summary* summary_out, void* stream) {
   fs_status s = check_common(ctx, dtype, h, W_shard, B, D, V_local);
   if (s != FS_OK) return s;
+  FS_LOCK(ctx);
   if (!summary_out) return fail(FS_ERR_INVALID, "summary_out is required");
   if (vocab_offset < 0 || V_total < vocab_offset + V_local || V_total >= (1LL << 31))
     return fail(FS_ERR_INVALID, "need 0 <= vocab_offset, vocab_offset + V_local <= V_total < 2^31");
@@ -805,6 +880,7 @@ static fs_status sample_logits_impl(fs_ctx* ctx, fs_dtype dtype, const void* log
                                     const uint64_t* seeds, const uint64_t* steps, int B, int V, int32_t* idx_out,
                                     float* score_out, float* logZ_out, float* logprob_out, void* stream) {
   if (!ctx) return fail(FS_ERR_INVALID, "ctx is NULL");
+  FS_LOCK(ctx);
   if (dtype != FS_BF16 && dtype != FS_F32) return fail(FS_ERR_INVALID, "unknown dtype");
   if (!logits || !idx_out) return fail(FS_ERR_INVALID, "logits and idx_out are required");
   if (B < 1 || V < 1 || ld < V) return fail(FS_ERR_INVALID, "need B >= 1, V >= 1, ld >= V");
@@ -848,6 +924,7 @@ fs_status fs_sample_logits_ex(fs_ctx* ctx, fs_dtype dtype, const void* logits, i
     if (a->top_k < 1 || a->top_k > fs::topk_max_k())
       return fail(FS_ERR_UNSUPPORTED, "top-k sampling needs 1 <= top_k <= 1024 (also required for top_p)");
     if (!ctx) return fail(FS_ERR_INVALID, "ctx is NULL");
+  FS_LOCK(ctx);
     if (dtype != FS_BF16 && dtype != FS_F32) return fail(FS_ERR_INVALID, "unknown dtype");
     if (!logits || !a->idx_out) return fail(FS_ERR_INVALID, "logits and idx_out are required");
     if (B < 1 || V < 1 || ld < V) return fail(FS_ERR_INVALID, "need B >= 1, V >= 1, ld >= V");
@@ -871,6 +948,7 @@ fs_status fs_sample_ex(fs_ctx* ctx, fs_dtype dtype, const void* h, const void* W
   if (!args) return fail(FS_ERR_INVALID, "args is NULL");
   fs_status s = check_common(ctx, dtype, h, W, B, D, V);
   if (s != FS_OK) return s;
+  FS_LOCK(ctx);
   if (!args->idx_out) return fail(FS_ERR_INVALID, "idx_out is required");
   if (args->steps && !args->seeds) return fail(FS_ERR_INVALID, "steps requires seeds");
   const bool use_p = args->top_p > 0.0f && args->top_p < 1.0f;
@@ -897,6 +975,7 @@ fs_status fs_sample_ex(fs_ctx* ctx, fs_dtype dtype, const void* h, const void* W
 
 fs_status fs_comm_window_create(fs_ctx* ctx, int world, int rank, int B_max, fs_ipc_handle* handle_out) {
   if (!ctx || !handle_out) return fail(FS_ERR_INVALID, "ctx and handle_out are required");
+  FS_LOCK(ctx);
   if (world < 1 || world > fs::kMaxWorld || rank < 0 || rank >= world || B_max < 1)
     return fail(FS_ERR_INVALID, "need 1 <= world <= 16, 0 <= rank < world, B_max >= 1");
   cudaError_t e = cudaSetDevice(ctx->device);
@@ -906,7 +985,7 @@ fs_status fs_comm_window_create(fs_ctx* ctx, int world, int rank, int B_max, fs_
   ctx->comm_off_flags = (rec + 127) & ~size_t(127);
   ctx->comm_off_acks = ctx->comm_off_flags + (((size_t)2 * world * 8 + 127) & ~size_t(127));
   ctx->comm_off_status = ctx->comm_off_acks + (((size_t)world * 8 + 127) & ~size_t(127));
-  const size_t bytes = ctx->comm_off_status + 128;
+  const size_t bytes = ctx->comm_off_status + 128;   // status: [0] timeouts, [64] push block counter
   if ((e = cudaMalloc(&ctx->comm_win, bytes)) != cudaSuccess) return fail(FS_ERR_OOM, "window cudaMalloc failed");
   if ((e = cudaMemset(ctx->comm_win, 0, bytes)) != cudaSuccess) return cuda_fail(e, "window memset");
   if ((e = cudaMalloc(&ctx->comm_local, (size_t)B_max * sizeof(fs_summary))) != cudaSuccess)
@@ -925,6 +1004,7 @@ fs_status fs_comm_window_create(fs_ctx* ctx, int world, int rank, int B_max, fs_
 
 fs_status fs_comm_window_open(fs_ctx* ctx, const fs_ipc_handle* handles) {
   if (!ctx || !handles) return fail(FS_ERR_INVALID, "ctx and handles are required");
+  FS_LOCK(ctx);
   if (!ctx->comm_win) return fail(FS_ERR_INVALID, "fs_comm_window_create first");
   cudaError_t e = cudaSetDevice(ctx->device);
   if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
@@ -937,12 +1017,23 @@ fs_status fs_comm_window_open(fs_ctx* ctx, const fs_ipc_handle* handles) {
       return cuda_fail(e, "cudaIpcOpenMemHandle");
     ctx->comm_peer[p] = static_cast<char*>(ptr);
   }
+  fs::PeerTab tab{};
+  for (int p = 0; p < ctx->comm_world; ++p) {
+    tab.rec[p] = reinterpret_cast<fs_summary*>(ctx->comm_peer[p]);
+    tab.flags[p] = reinterpret_cast<uint64_t*>(ctx->comm_peer[p] + ctx->comm_off_flags);
+    tab.acks[p] = reinterpret_cast<uint64_t*>(ctx->comm_peer[p] + ctx->comm_off_acks);
+  }
+  if (!ctx->comm_peertab && (e = cudaMalloc(&ctx->comm_peertab, sizeof(tab))) != cudaSuccess)
+    return fail(FS_ERR_OOM, "peer table cudaMalloc failed");
+  if ((e = cudaMemcpy(ctx->comm_peertab, &tab, sizeof(tab), cudaMemcpyHostToDevice)) != cudaSuccess)
+    return cuda_fail(e, "peer table upload");
   ctx->comm_open = true;
   return FS_OK;
 }
 
 fs_status fs_comm_window_destroy(fs_ctx* ctx) {
   if (!ctx) return fail(FS_ERR_INVALID, "ctx is NULL");
+  FS_LOCK(ctx);
   cudaSetDevice(ctx->device);
   if (ctx->comm_open)
     for (int p = 0; p < ctx->comm_world; ++p)
@@ -951,8 +1042,10 @@ fs_status fs_comm_window_destroy(fs_ctx* ctx) {
   ctx->comm_open = false;
   if (ctx->comm_win) cudaFree(ctx->comm_win);
   if (ctx->comm_local) cudaFree(ctx->comm_local);
+  if (ctx->comm_peertab) cudaFree(ctx->comm_peertab);
   ctx->comm_win = nullptr;
   ctx->comm_local = nullptr;
+  ctx->comm_peertab = nullptr;
   ctx->comm_world = 0;
   return FS_OK;
 }
@@ -962,10 +1055,33 @@ fs_status fs_sample_tp_push(fs_ctx* ctx, fs_dtype dtype, const void* h, const vo
                             int V_local, int64_t vocab_offset, int64_t V_total, int32_t* idx_out, float* score_out,
                             float* logZ_out, void* stream) {
   if (!ctx || !ctx->comm_open) return fail(FS_ERR_INVALID, "open the exchange window first (fs_comm_window_open)");
+  FS_LOCK(ctx);
   if (!idx_out) return fail(FS_ERR_INVALID, "idx_out is required");
   if (B > ctx->comm_bmax) return fail(FS_ERR_INVALID, "B exceeds the window's B_max");
-  fs_status s = fs_sample_shard(ctx, dtype, h, W_shard, bias_shard, temperature, mask, seed, step, B, D, V_local,
-                                vocab_offset, V_total, ctx->comm_local, stream);
+  fs_status s = check_common(ctx, dtype, h, W_shard, B, D, V_local);
+  if (s != FS_OK) return s;
+  if (vocab_offset < 0 || V_total < vocab_offset + V_local || V_total >= (1LL << 31))
+    return fail(FS_ERR_INVALID, "need 0 <= vocab_offset, vocab_offset + V_local <= V_total < 2^31");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned* status = reinterpret_cast<unsigned*>(ctx->comm_win + ctx->comm_off_status);
+  const uint64_t epoch = ++ctx->comm_epoch;
+  if (B <= 256) {
+    // fused: the shard sampler's last reduction step (the last stage-1 CTA for B <= 16, else the
+    // stage-2 row reduce) stores the records into every peer window and releases the flags; one
+    // PDL-chained block then waits for the n flags and combines
+    const fs::PushCtx pc{ctx->comm_peertab, ctx->comm_world, ctx->comm_rank, ctx->comm_bmax, epoch, status + 16,
+                         status};
+    PathArgs a{dtype, h, W_shard, bias_shard, temperature, mask, (V_total + 31) / 32, seed, step, B, D, V_local,
+               vocab_offset, ((V_local + 127) / 128) * 128, true, nullptr, nullptr, nullptr, ctx->comm_local, 1,
+               nullptr};
+    a.push = &pc;
+    if ((s = run_path(ctx, a, st)) != FS_OK) return s;
+    cudaError_t e = fs::launch_exchange_wait(ctx->comm_peertab, ctx->comm_world, ctx->comm_rank, B, ctx->comm_bmax,
+                                             epoch, idx_out, score_out, logZ_out, status, st, ctx->pdl != 0);
+    return e == cudaSuccess ? FS_OK : cuda_fail(e, "exchange wait kernel launch");
+  }
+  s = fs_sample_shard(ctx, dtype, h, W_shard, bias_shard, temperature, mask, seed, step, B, D, V_local, vocab_offset,
+                      V_total, ctx->comm_local, stream);
   if (s != FS_OK) return s;
   fs::PeerTab peers{};
   for (int p = 0; p < ctx->comm_world; ++p) {
@@ -973,12 +1089,99 @@ fs_status fs_sample_tp_push(fs_ctx* ctx, fs_dtype dtype, const void* h, const vo
     peers.flags[p] = reinterpret_cast<uint64_t*>(ctx->comm_peer[p] + ctx->comm_off_flags);
     peers.acks[p] = reinterpret_cast<uint64_t*>(ctx->comm_peer[p] + ctx->comm_off_acks);
   }
-  const uint64_t epoch = ++ctx->comm_epoch;
   cudaError_t e = fs::launch_exchange_combine(ctx->comm_local, peers, ctx->comm_world, ctx->comm_rank, B,
-                                              ctx->comm_bmax, epoch, idx_out, score_out, logZ_out,
-                                              reinterpret_cast<unsigned*>(ctx->comm_win + ctx->comm_off_status),
-                                              static_cast<cudaStream_t>(stream), ctx->pdl != 0);
+                                              ctx->comm_bmax, epoch, idx_out, score_out, logZ_out, status, st,
+                                              ctx->pdl != 0);
   return e == cudaSuccess ? FS_OK : cuda_fail(e, "exchange kernel launch");
+}
+
+fs_status fs_comm_unique_id(void* id_out) {
+  if (!id_out) return fail(FS_ERR_INVALID, "id_out is required");
+  const fs::NcclApi& nc = fs::nccl_api();
+  if (!nc.ok) return fail(FS_ERR_UNSUPPORTED, std::string("NCCL unavailable: ") + nc.why);
+  ncclUniqueId id;
+  const ncclResult_t r = nc.GetUniqueId(&id);
+  if (r != ncclSuccess) return fail(FS_ERR_NCCL, std::string("ncclGetUniqueId: ") + nc.GetErrorString(r));
+  std::memcpy(id_out, &id, sizeof(id));
+  return FS_OK;
+}
+
+fs_status fs_comm_init(fs_ctx* ctx, const void* nccl_unique_id, int world, int rank) {
+  if (!ctx || !nccl_unique_id) return fail(FS_ERR_INVALID, "ctx and nccl_unique_id are required");
+  FS_LOCK(ctx);
+  if (world < 1 || rank < 0 || rank >= world) return fail(FS_ERR_INVALID, "need world >= 1, 0 <= rank < world");
+  const fs::NcclApi& nc = fs::nccl_api();
+  if (!nc.ok) return fail(FS_ERR_UNSUPPORTED, std::string("NCCL unavailable: ") + nc.why);
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  fs_comm_destroy(ctx);
+  ncclUniqueId id;
+  std::memcpy(&id, nccl_unique_id, sizeof(id));
+  const ncclResult_t r = nc.CommInitRank(&ctx->nccl, world, id, rank);
+  if (r != ncclSuccess) {
+    ctx->nccl = nullptr;
+    return fail(FS_ERR_NCCL, std::string("ncclCommInitRank: ") + nc.GetErrorString(r));
+  }
+  ctx->nccl_world = world;
+  ctx->nccl_rank = rank;
+  return FS_OK;
+}
+
+fs_status fs_comm_destroy(fs_ctx* ctx) {
+  if (!ctx) return fail(FS_ERR_INVALID, "ctx is NULL");
+  FS_LOCK(ctx);
+  if (ctx->nccl) {
+    cudaSetDevice(ctx->device);
+    fs::nccl_api().CommDestroy(ctx->nccl);
+  }
+  if (ctx->tp_buf) cudaFree(ctx->tp_buf);
+  ctx->nccl = nullptr;
+  ctx->tp_buf = nullptr;
+  ctx->tp_bmax = 0;
+  ctx->nccl_world = 0;
+  return FS_OK;
+}
+
+fs_status fs_sample_tp(fs_ctx* ctx, fs_dtype dtype, const void* h, const void* W_shard, const float* bias_shard,
+                       const float* temperature, const uint32_t* mask, uint64_t seed, uint64_t step, int B, int D,
+                       int V_local, int64_t vocab_offset, int64_t V_total, int32_t* idx_out, float* score_out,
+                       float* logZ_out, fs_summary* per_rank_out, void* stream) {
+  if (!ctx) return fail(FS_ERR_INVALID, "ctx is NULL");
+  FS_LOCK(ctx);
+  if (!ctx->nccl) return fail(FS_ERR_INVALID, "no communicator: call fs_comm_init first");
+  if (!idx_out) return fail(FS_ERR_INVALID, "idx_out is required");
+  const fs::NcclApi& nc = fs::nccl_api();
+  // an error of an earlier asynchronous collective surfaces here
+  ncclResult_t ar = ncclSuccess;
+  ncclResult_t r = nc.CommGetAsyncError(ctx->nccl, &ar);
+  if (r != ncclSuccess || (ar != ncclSuccess && ar != ncclInProgress))
+    return fail(FS_ERR_NCCL, std::string("NCCL communicator error: ") + nc.GetErrorString(r != ncclSuccess ? r : ar));
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  const int world = ctx->nccl_world;
+  if (B > ctx->tp_bmax) {
+    if (ctx->tp_buf) cudaFree(ctx->tp_buf);
+    ctx->tp_buf = nullptr;
+    ctx->tp_bmax = 0;
+    if ((e = cudaMalloc(&ctx->tp_buf, (size_t)(1 + world) * B * sizeof(fs_summary))) != cudaSuccess)
+      return fail(FS_ERR_OOM, "TP summary buffer cudaMalloc failed");
+    ctx->tp_bmax = B;
+  }
+  fs_summary* local = ctx->tp_buf;
+  fs_summary* gathered = ctx->tp_buf + ctx->tp_bmax;
+  fs_status s = fs_sample_shard(ctx, dtype, h, W_shard, bias_shard, temperature, mask, seed, step, B, D, V_local,
+                                vocab_offset, V_total, local, stream);
+  if (s != FS_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // Alg. A.4 line 4: every rank contributes its B x 12-byte message; [world][B] arrives
+  r = nc.AllGather(local, gathered, (size_t)B * sizeof(fs_summary), ncclUint8, ctx->nccl, st);
+  if (r != ncclSuccess) return fail(FS_ERR_NCCL, std::string("ncclAllGather: ") + nc.GetErrorString(r));
+  e = fs::launch_combine(gathered, world, B, idx_out, score_out, logZ_out, st);
+  if (e != cudaSuccess) return cuda_fail(e, "combine launch");
+  if (per_rank_out && (e = cudaMemcpyAsync(per_rank_out, gathered, (size_t)world * B * sizeof(fs_summary),
+                                           cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+    return cuda_fail(e, "per-rank summary copy");
+  return FS_OK;
 }
 
 fs_status fs_combine_summaries(const fs_summary* gathered, int n, int B, int32_t* idx_out, float* score_out,
@@ -1004,6 +1207,7 @@ fs_status fs_random_bits(uint64_t seed, uint64_t step, uint32_t tag, const int32
 
 fs_status fs_copy_async(fs_ctx* ctx, void* dst, const void* src, size_t bytes, void* stream) {
   if (!ctx) return fail(FS_ERR_INVALID, "ctx is required");
+  FS_LOCK(ctx);
   if (bytes == 0) return FS_OK;
   if (!dst || !src) return fail(FS_ERR_INVALID, "dst and src are required");
   if ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15u)
@@ -1015,7 +1219,8 @@ fs_status fs_copy_async(fs_ctx* ctx, void* dst, const void* src, size_t bytes, v
     return fail(FS_ERR_INVALID, "src must be pinned host memory or device memory");
   e = cudaSetDevice(ctx->device);
   if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
-  e = fs::launch_copy_in(dst, src, bytes, ctx->pdl_w && ctx->pdl, static_cast<cudaStream_t>(stream));
+  e = fs::launch_copy_in(dst, src, bytes, ctx->pdl_w && ctx->pdl, at.type == cudaMemoryTypeHost,
+                         static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? FS_OK : cuda_fail(e, "copy kernel launch");
 }
 

@@ -14,6 +14,7 @@
 #pragma once
 #include "../../include/flashsample.h"
 #include "fs_device.cuh"
+#include "fs_peer.cuh"
 #include "fs_sm100.cuh"
 
 namespace fs {
@@ -119,7 +120,7 @@ __device__ __forceinline__ void epi_columns(const float* acc, int col0, const Ro
     for (int jj = 0; jj < 4; ++jj) {
       const int b = b0 + jj;
       float lt = (acc[j + jj] + ra.bias) * ea.invtau[b];
-      if (ea.mask != nullptr && b < ea.B) {
+      if (ea.mask != nullptr && b < ea.B && ra.valid) {     // padding rows past V read no mask word
         const uint32_t w = __ldg(ea.mask + (int64_t)b * ea.mask_words + (ra.v_global >> 5));
         if (!((w >> (ra.v_global & 31)) & 1u)) lt = -INFINITY;
       }
@@ -376,6 +377,9 @@ __device__ __forceinline__ unsigned long long pack_state(const State& s) {
 // Called by all `nthr` epilogue threads (ids et) of every CTA after their atomicMax calls: the last
 // CTA to arrive (threadFenceReduction pattern) converts the row maxima to (idx, score) exactly as
 // stage 2's to_summary does, and leaves fin_best / fin_ctr at 0 for the next call.
+// With in-kernel staging (h_bar != nullptr), h_bar[1] is the staging-timeout flag (wait_h_staged):
+// when set, h was not fully staged before some CTA's first h load, so every row is reported
+// undefined (idx -1, score -inf) and h_bar[2] counts the event (fs_ctx_query "staging_timeouts").
 __device__ __forceinline__ void finalize_last_cta(unsigned long long* best, unsigned int* ctr, int B,
                                                   int32_t* idx_out, float* score_out, int et, int nthr,
                                                   uint32_t bar_id, volatile int* flag, unsigned n_ctas,
@@ -386,16 +390,24 @@ __device__ __forceinline__ void finalize_last_cta(unsigned long long* best, unsi
   sm100::named_bar_sync(bar_id, nthr);
   if (*flag) {
     __threadfence();
+    const bool timed_out = h_bar != nullptr && *reinterpret_cast<volatile unsigned int*>(h_bar + 1) != 0u;
     for (int b = et; b < B; b += nthr) {
       const unsigned long long v = atomicExch(&best[b], 0ull);
       const uint32_t key = (uint32_t)(v >> 32);
-      const bool defined = key > kKeyNegInf;
+      const bool defined = key > kKeyNegInf && !timed_out;
       idx_out[b] = defined ? (int32_t)~(uint32_t)v : -1;
       if (score_out) score_out[b] = defined ? key_to_float(key) : -INFINITY;
     }
+    sm100::named_bar_sync(bar_id, nthr);     // every thread read the timeout flag
     if (et == 0) {
       atomicExch(ctr, 0u);
-      if (h_bar) atomicExch(h_bar, 0u);      // every CTA passed the staging barrier long ago
+      if (h_bar) {
+        atomicExch(h_bar, 0u);               // every CTA passed the staging barrier long ago
+        if (timed_out) {
+          atomicExch(h_bar + 1, 0u);
+          atomicAdd(h_bar + 2, 1u);
+        }
+      }
     }
   }
 }
@@ -419,9 +431,11 @@ __device__ __forceinline__ float logprob_of(const State& s) {
 // Stage 2 of one batch row b (Alg. 2; App. E), one warp: lane L merges slots L, L+32, ...
 // (L2 loads, so a last CTA of the same grid may call it), then a fixed xor tree -- deterministic,
 // so logZ is bit-reproducible and identical whichever kernel runs it.
+// With `push` (f2), the row's summary record is also stored into every peer's exchange window.
 __device__ __forceinline__ void reduce_row(const State* part, const int* part_group, int n_slots, int B, int b,
                                            int lane, int32_t* idx_out, float* score_out, float* logZ_out,
-                                           fs_summary* groups_out, float* logprob_out) {
+                                           fs_summary* groups_out, float* logprob_out,
+                                           const PushCtx* push = nullptr) {
   State acc = state_empty();
 #pragma unroll 4
   for (int s = lane; s < n_slots; s += 32)
@@ -445,26 +459,41 @@ __device__ __forceinline__ void reduce_row(const State* part, const int* part_gr
     if (logZ_out) logZ_out[b] = f.log_mass;
     if (groups_out) groups_out[b] = f;
     if (logprob_out) logprob_out[b] = logprob_of(acc);
+    if (push) push_record(*push, b, f);
   }
 }
 
 // One-kernel finalize with log-mass (single group, small B): every CTA has written its candidate
 // slot (part, part_group); the last CTA to arrive runs stage 2's reduce_row for every row, one warp
 // per row, and resets the counter.
+// With push.peers (f2, a TP shard step) the same CTA stores every row's summary into the peers'
+// exchange windows and releases this rank's flags: the exchange needs no extra kernel before the
+// wait + combine.
 __device__ __forceinline__ void finalize_lse_last_cta(const State* part, const int* part_group, int B,
                                                       unsigned int* ctr, int32_t* idx_out, float* score_out,
                                                       float* logZ_out, fs_summary* groups_out, float* logprob_out,
-                                                      int et, int nthr, uint32_t bar_id, volatile int* flag) {
+                                                      int et, int nthr, uint32_t bar_id, volatile int* flag,
+                                                      const PushCtx& push) {
   __threadfence();
   sm100::named_bar_sync(bar_id, nthr);
   if (et == 0) *flag = (atomicAdd(ctr, 1u) == gridDim.x - 1) ? 1 : 0;
   sm100::named_bar_sync(bar_id, nthr);
   if (*flag) {
     __threadfence();
+    const bool pushing = push.peers != nullptr;
+    if (pushing) {                             // readers are done with this parity slot
+      push_wait_readers(push, et);
+      sm100::named_bar_sync(bar_id, nthr);
+    }
     const int w = et >> 5, nw = nthr >> 5, lane = et & 31;
     for (int b = w; b < B; b += nw)
-      reduce_row(part, part_group, gridDim.x, B, b, lane, idx_out, score_out, logZ_out, groups_out, logprob_out);
-    if (et == 0) atomicExch(ctr, 0u);
+      reduce_row(part, part_group, gridDim.x, B, b, lane, idx_out, score_out, logZ_out, groups_out, logprob_out,
+                 pushing ? &push : nullptr);
+    if (pushing) sm100::named_bar_sync(bar_id, nthr);
+    if (et == 0) {
+      atomicExch(ctr, 0u);
+      if (pushing) push_release(push);
+    }
   }
 }
 
@@ -487,13 +516,19 @@ __device__ __forceinline__ void stage_h_slice(const void* h_host, const void* h_
   if (et == 0) atomicAdd(h_bar, 1u);
 }
 // Producer side: wait until every CTA staged its slice, then order the TMA reads after it.
-// Bounded: if the grid's CTAs cannot all be resident (a shared GPU), trap after ~10 s instead of
-// hanging -- the launch then fails with an error the caller sees.
-__device__ __forceinline__ void wait_h_staged(const unsigned int* h_bar) {
+// The host launches in-kernel staging only when the whole grid fits on the device at once
+// (fs_api.cu run_path); should the CTAs still not be co-resident (a GPU shared through MPS or
+// green contexts), the wait gives up after ~5 s instead of hanging or trapping: it raises the
+// timeout flag h_bar[1] and proceeds, the CTAs drain, and the finalizing CTA reports every row
+// as undefined (finalize_last_cta) -- a recoverable per-call failure, no sticky CUDA error.
+__device__ __forceinline__ void wait_h_staged(unsigned int* h_bar) {
   const uint64_t t0 = sm100::globaltimer();
   while (sm100::ld_acquire_gpu(h_bar) < gridDim.x) {
     __nanosleep(64);
-    if (sm100::globaltimer() - t0 > 10000000000ull) __trap();
+    if (sm100::globaltimer() - t0 > 5000000000ull) {
+      atomicExch(h_bar + 1, 1u);
+      break;
+    }
   }
   sm100::fence_proxy_async_global();
 }

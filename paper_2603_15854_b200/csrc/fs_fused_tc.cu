@@ -365,7 +365,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
       if (!p.fin_best && p.fin_lse)
         finalize_lse_last_cta(p.part, p.part_group, p.B, p.fin_ctr, p.idx_out, p.score_out, p.logZ_out,
                               p.groups_out, p.logprob_out, et, 32 * kEpiWarps, 1,
-                              reinterpret_cast<volatile int*>(scratch + kEpiWarps * BN));
+                              reinterpret_cast<volatile int*>(scratch + kEpiWarps * BN), p.push);
       if (p.dbg_times && et == 0) p.dbg_times[blockIdx.x * 8 + 5] = sm100::globaltimer();
     }
   }
@@ -408,15 +408,36 @@ cudaError_t launch_fused_tc_topk(const CUtensorMap& hmap, const StageOneParams& 
   const bool xform = p.bias || p.temperature || p.mask;
   auto kern = p.mode == 2 ? fused_tc_kernel<false, false, false, 2>
                           : xform ? fused_tc_kernel<false, true, false, 1> : fused_tc_kernel<false, false, false, 1>;
-  static bool attr_set[3] = {false, false, false};
-  const int variant = p.mode == 2 ? 2 : xform ? 1 : 0;
-  if (!attr_set[variant]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_set[variant] = true;
-  }
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), 227 * 1024);
+  if (e != cudaSuccess) return e;
   kern<<<grid, kThreadsTC, smem, stream>>>(hmap, p);
   return cudaGetLastError();
+}
+
+using TcKern = void (*)(const CUtensorMap, const StageOneParams);
+
+static TcKern pick_tc_kernel(const StageOneParams& p, bool lse) {
+  const bool xform = p.bias || p.temperature || p.mask || p.seeds;
+  const bool prq = p.seeds != nullptr;
+  return lse ? (prq ? fused_tc_kernel<true, true, true> : xform ? fused_tc_kernel<true, true, false> : fused_tc_kernel<true, false, false>)
+             : (prq ? fused_tc_kernel<false, true, true> : xform ? fused_tc_kernel<false, true, false> : fused_tc_kernel<false, false, false>);
+}
+
+static size_t tc_smem_bytes(const StageOneParams& p, int BN) {
+  return 1024 + (size_t)p.stages * p.kbps * (kWStageBytes + BN * kBlockK * 2) + kExtraBytes;
+}
+
+cudaError_t fused_tc_resident(const StageOneParams& p, int BN, bool lse, int* ctas) {
+  TcKern kern = pick_tc_kernel(p, lse);
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), 227 * 1024);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0, dev = 0, sms = 0;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreadsTC, tc_smem_bytes(p, BN))) != cudaSuccess)
+    return e;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  *ctas = per_sm * sms;
+  return cudaSuccess;
 }
 
 cudaError_t launch_fused_tc(const CUtensorMap& hmap, const StageOneParams& p_in, int BN, bool lse, int grid,
@@ -424,22 +445,13 @@ cudaError_t launch_fused_tc(const CUtensorMap& hmap, const StageOneParams& p_in,
   StageOneParams p = p_in;
   p.bn = BN;
   p.tmem_cols = tmem_cols_for(BN);
-  const size_t smem = 1024 + (size_t)p.stages * p.kbps * (kWStageBytes + BN * kBlockK * 2) + kExtraBytes;
-  const bool xform = p.bias || p.temperature || p.mask || p.seeds;
-  const bool prq = p.seeds != nullptr;
-  auto kern = lse ? (prq ? fused_tc_kernel<true, true, true> : xform ? fused_tc_kernel<true, true, false> : fused_tc_kernel<true, false, false>)
-                  : (prq ? fused_tc_kernel<false, true, true> : xform ? fused_tc_kernel<false, true, false> : fused_tc_kernel<false, false, false>);
-  static bool attr_set[8] = {false, false, false, false, false, false, false, false};
-  const int variant = (lse ? 4 : 0) + (prq ? 2 : 0) + (xform ? 1 : 0);
-  if (!attr_set[variant]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_set[variant] = true;
-  }
+  TcKern kern = pick_tc_kernel(p, lse);
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), 227 * 1024);
+  if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreadsTC);
-  cfg.dynamicSmemBytes = smem;
+  cfg.dynamicSmemBytes = tc_smem_bytes(p, BN);
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

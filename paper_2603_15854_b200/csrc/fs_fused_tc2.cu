@@ -82,12 +82,16 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
     }
     sm100::fence_barrier_init();
   }
-  if (warp == 1) sm100::tmem_alloc_pair(tmem_slot, (uint32_t)p.tmem_cols);
+  // Each CTA of the pair passes its own slot word (tmem_slot[rank]) to the collective
+  // cta_group::2 allocation, so the two CTAs' allocator writes never target the same shared-memory
+  // word even where the paired allocator writes through the cluster window (racecheck reported the
+  // shared slot as a write-write hazard between the pair).
+  if (warp == 1) sm100::tmem_alloc_pair(tmem_slot + rank, (uint32_t)p.tmem_cols);
   sm100::tc_fence_before();
   sm100::cluster_sync();                    // both CTAs' barriers exist before any remote signal
   __syncthreads();                          // CTA-level order for the allocator's smem write (racecheck)
   sm100::tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_base = tmem_slot[rank];
   sm100::pdl_launch_dependents();
   if (warp != 0) {
     // every input but W is read past the dependency wait (the producer defers only its h loads)
@@ -286,7 +290,7 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
       if (!p.fin_best && p.fin_lse)
         finalize_lse_last_cta(p.part, p.part_group, p.B, p.fin_ctr, p.idx_out, p.score_out, p.logZ_out,
                               p.groups_out, p.logprob_out, et, 32 * kEpiWarps, 1,
-                              reinterpret_cast<volatile int*>(scratch + kSlotWarps * BN));
+                              reinterpret_cast<volatile int*>(scratch + kSlotWarps * BN), p.push);
       if (p.dbg_times && et == 0) p.dbg_times[blockIdx.x * 8 + 5] = sm100::globaltimer();
     }
   }
@@ -307,29 +311,22 @@ int tc2_stages(int BN, int kbps) {
   return S;
 }
 
-cudaError_t launch_fused_tc2(const CUtensorMap& hmap, const StageOneParams& p_in, int BN, bool lse, int grid,
-                             cudaStream_t stream) {
-  StageOneParams p = p_in;
-  p.bn = BN;
-  p.tmem_cols = tmem_cols_for(BN);
-  const size_t smem = 1024 + (size_t)p.stages * p.kbps * (kWBytes + (BN / 2) * kBlockK * 2) + kExtraBytes;
+using Tc2Kern = void (*)(const CUtensorMap, const StageOneParams);
+
+static Tc2Kern pick_tc2_kernel(const StageOneParams& p, bool lse) {
   const bool xform = p.bias || p.temperature || p.mask || p.seeds;
   const bool prq = p.seeds != nullptr;
-  auto kern = lse ? (prq ? fused_tc2_kernel<true, true, true> : xform ? fused_tc2_kernel<true, true, false> : fused_tc2_kernel<true, false, false>)
-                  : (prq ? fused_tc2_kernel<false, true, true> : xform ? fused_tc2_kernel<false, true, false> : fused_tc2_kernel<false, false, false>);
-  static bool attr_set[8] = {false, false, false, false, false, false, false, false};
-  const int variant = (lse ? 4 : 0) + (prq ? 2 : 0) + (xform ? 1 : 0);
-  if (!attr_set[variant]) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    if (e != cudaSuccess) return e;
-    attr_set[variant] = true;
-  }
+  return lse ? (prq ? fused_tc2_kernel<true, true, true> : xform ? fused_tc2_kernel<true, true, false> : fused_tc2_kernel<true, false, false>)
+             : (prq ? fused_tc2_kernel<false, true, true> : xform ? fused_tc2_kernel<false, true, false> : fused_tc2_kernel<false, false, false>);
+}
+
+static cudaLaunchConfig_t tc2_config(const StageOneParams& p, int BN, int grid, cudaStream_t stream,
+                                     cudaLaunchAttribute (&attr)[2]) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = smem;
+  cfg.dynamicSmemBytes = 1024 + (size_t)p.stages * p.kbps * (kWBytes + (BN / 2) * kBlockK * 2) + kExtraBytes;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 2;
   attr[0].val.clusterDim.y = 1;
@@ -338,6 +335,32 @@ cudaError_t launch_fused_tc2(const CUtensorMap& hmap, const StageOneParams& p_in
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = p.pdl_w ? 2 : 1;
+  return cfg;
+}
+
+cudaError_t fused_tc2_resident(const StageOneParams& p, int BN, bool lse, int grid, int* ctas) {
+  Tc2Kern kern = pick_tc2_kernel(p, lse);
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), 227 * 1024);
+  if (e != cudaSuccess) return e;
+  cudaLaunchAttribute attr[2];
+  cudaLaunchConfig_t cfg = tc2_config(p, BN, grid, nullptr, attr);
+  cfg.numAttrs = 1;
+  int clusters = 0;
+  if ((e = cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg)) != cudaSuccess) return e;
+  *ctas = 2 * clusters;
+  return cudaSuccess;
+}
+
+cudaError_t launch_fused_tc2(const CUtensorMap& hmap, const StageOneParams& p_in, int BN, bool lse, int grid,
+                             cudaStream_t stream) {
+  StageOneParams p = p_in;
+  p.bn = BN;
+  p.tmem_cols = tmem_cols_for(BN);
+  Tc2Kern kern = pick_tc2_kernel(p, lse);
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), 227 * 1024);
+  if (e != cudaSuccess) return e;
+  cudaLaunchAttribute attr[2];
+  cudaLaunchConfig_t cfg = tc2_config(p, BN, grid, stream, attr);
   return cudaLaunchKernelEx(&cfg, kern, hmap, p);
 }
 

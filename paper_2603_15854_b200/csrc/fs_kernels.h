@@ -3,10 +3,30 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <mutex>
+#include <set>
+#include <utility>
 
 #include "../../include/flashsample.h"
+#include "fs_peer.cuh"
 
 namespace fs {
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-(function, device) setting: set it once for
+// every device a kernel is launched on (the current device), under a lock (several host threads
+// may launch at once).
+inline cudaError_t ensure_smem_attr(const void* kern, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count({kern, dev})) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert({kern, dev});
+  return e;
+}
 
 struct State;
 struct Cand;
@@ -72,6 +92,8 @@ struct StageOneParams {
   unsigned int* h_bar;            // grid-barrier counter (reset by the finalizing CTA)
   int pdl_w;                      // launched with PDL: W loads may precede griddepcontrol.wait;
                                   // everything else (h, bias, tau, mask, seeds, outputs) follows it
+  PushCtx push;                   // f2: the finalizing CTA also pushes the shard summaries to every
+                                  // peer window and releases the flags (push.peers == nullptr: off)
 };
 
 
@@ -85,6 +107,11 @@ cudaError_t launch_fused_tc2(const CUtensorMap& hmap, const StageOneParams& p, i
                              cudaStream_t stream);
 cudaError_t launch_fused_tc(const CUtensorMap& hmap, const StageOneParams& p, int BN, bool lse, int grid,
                             cudaStream_t stream);
+// How many CTAs of the stage-1 kernel that launch_fused_tc / launch_fused_tc2 would pick for `p`
+// can be resident on the current device at once (occupancy API; the pair kernel counts clusters).
+// In-kernel staging (a grid barrier) is only used when the whole grid fits.
+cudaError_t fused_tc_resident(const StageOneParams& p, int BN, bool lse, int* ctas);
+cudaError_t fused_tc2_resident(const StageOneParams& p, int BN, bool lse, int grid, int* ctas);
 // p.mode 1 / 2 of the 1-CTA kernel (top-k candidates / raw logits); xform applies to mode 1.
 cudaError_t launch_fused_tc_topk(const CUtensorMap& hmap, const StageOneParams& p, int BN, int grid,
                                  cudaStream_t stream);
@@ -109,7 +136,8 @@ cudaError_t launch_reduce(const State* part, const int* part_group, const SlotLa
                           cudaStream_t stream, bool pdl, float* logprob_out = nullptr,
                           const int* grp_lo = nullptr,    // [n_groups+1] first slot per group (host-computed)
                           State* gscratch = nullptr,      // [B][n_groups] group states (warp-per-group kernel)
-                          int* row_ctr = nullptr);        // [B] zeroed counters (warp-per-group kernel)
+                          int* row_ctr = nullptr,         // [B] zeroed counters (warp-per-group kernel)
+                          const PushCtx* push = nullptr); // single group: also push the records (f2)
 // Standalone sampler over materialised logits [B][ld] (bf16 or fp32): candidates per (V-block, row).
 cudaError_t launch_logits_sample(fs_dtype dtype, const void* logits, int64_t ld, const float* bias,
                                  const float* temperature, const uint32_t* mask, int64_t mask_words, int B, int V,
@@ -143,17 +171,15 @@ cudaError_t launch_topk_final(const Cand* cand, int ncand, int* row_count, int B
                               const uint64_t* steps, int32_t* idx_out, float* score_out, float* logZ_out,
                               float* logprob_out, cudaStream_t stream, int row_offset, bool pdl,
                               const uint32_t* slot_lb, int nslots, int m);
-// Peer windows of the f2 exchange (fs_reduce.cu): per rank, records [2][world][B_max], flags
-// [2][world] and acks [world] (see include/flashsample.h fs_comm_window_create).
-constexpr int kMaxWorld = 16;
-struct PeerTab {
-  fs_summary* rec[kMaxWorld];
-  uint64_t* flags[kMaxWorld];
-  uint64_t* acks[kMaxWorld];
-};
+// f2 exchange, unfused form (B > 256): push `local` [B] into every peer window, wait, combine.
 cudaError_t launch_exchange_combine(const fs_summary* local, const PeerTab& peers, int world, int rank, int B,
                                     int B_max, uint64_t epoch, int32_t* idx_out, float* score_out, float* logZ_out,
                                     unsigned* timeouts, cudaStream_t stream, bool pdl);
+// f2 exchange, fused form: the records were pushed by the shard sampler itself (PushCtx); this
+// one-block kernel (PDL) only acquires the n flags of `epoch`, combines and acknowledges.
+cudaError_t launch_exchange_wait(const PeerTab* peers_dev, int world, int rank, int B, int B_max, uint64_t epoch,
+                                 int32_t* idx_out, float* score_out, float* logZ_out, unsigned* timeouts,
+                                 cudaStream_t stream, bool pdl);
 cudaError_t launch_combine(const fs_summary* gathered, int n, int B, int32_t* idx_out, float* score_out,
                            float* logZ_out, cudaStream_t stream);
 cudaError_t launch_merge(const fs_summary* a, const fs_summary* b, fs_summary* out, int count,
@@ -162,6 +188,7 @@ cudaError_t launch_random_bits(uint64_t seed, uint64_t step, uint32_t tag, const
                                uint32_t* r, int64_t n, cudaStream_t stream);
 cudaError_t launch_gumbel(const uint32_t* r, float* g, int64_t n, cudaStream_t stream);
 // Input staging copy (fs_copy_async): src loads before, dst stores after the PDL dependency wait.
-cudaError_t launch_copy_in(void* dst, const void* src, size_t bytes, bool pdl, cudaStream_t stream);
+// src_host: pinned host src (loads may precede the wait); device src is read after it.
+cudaError_t launch_copy_in(void* dst, const void* src, size_t bytes, bool pdl, bool src_host, cudaStream_t stream);
 
 }  // namespace fs

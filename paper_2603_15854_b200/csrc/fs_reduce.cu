@@ -32,15 +32,31 @@ constexpr int kReduceThreads = 256;
 // Single group (Alg. 2 stage 2; or one TP shard's summary): one warp per batch row,
 // each lane merges slots lane, lane+32, ... (independent loads in flight), then a fixed
 // shuffle tree -- deterministic, so logZ is bit-reproducible.
+// With push.peers (f2, a TP shard step) every row's record is also stored into the peers'
+// exchange windows; the last block to finish (counter push.ctr) releases this rank's flags.
 __global__ void __launch_bounds__(128)
 reduce_rows_kernel(const State* __restrict__ part, const int* __restrict__ part_group, int n_slots, int B,
                    int32_t* idx_out, float* score_out, float* logZ_out, fs_summary* groups_out,
-                   float* logprob_out) {
+                   float* logprob_out, PushCtx push) {
   sm100::pdl_wait();                       // stage-1 results are visible past this point
   const int lane = threadIdx.x & 31;
   const int b = blockIdx.x * 4 + (threadIdx.x >> 5);
-  if (b >= B) return;
-  reduce_row(part, part_group, n_slots, B, b, lane, idx_out, score_out, logZ_out, groups_out, logprob_out);
+  const bool pushing = push.peers != nullptr;
+  if (pushing) {                           // readers are done with this parity slot
+    push_wait_readers(push, threadIdx.x);
+    __syncthreads();
+  }
+  if (b < B)
+    reduce_row(part, part_group, n_slots, B, b, lane, idx_out, score_out, logZ_out, groups_out, logprob_out,
+               pushing ? &push : nullptr);
+  if (pushing) {
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(push.ctr, 1u) == gridDim.x - 1) {
+      push_release(push);                  // every block's records are visible (fence + counter)
+      atomicExch(push.ctr, 0u);
+    }
+  }
 }
 
 // Grouped variant (§4.1, App. E): one block per batch row, one thread per group.  Slots are
@@ -211,7 +227,7 @@ __global__ void gumbel_kernel(const uint32_t* r, float* g, int64_t n) {
 cudaError_t launch_reduce(const State* part, const int* part_group, const SlotLayout& lay, int B, int n_groups,
                           int32_t* idx_out, float* score_out, float* logZ_out, fs_summary* groups_out,
                           cudaStream_t stream, bool pdl, float* logprob_out, const int* grp_lo,
-                          State* gscratch, int* row_ctr) {
+                          State* gscratch, int* row_ctr, const PushCtx* push) {
   cudaLaunchConfig_t cfg = {};
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -222,8 +238,10 @@ cudaError_t launch_reduce(const State* part, const int* part_group, const SlotLa
   if (n_groups == 1) {
     cfg.gridDim = dim3((B + 3) / 4);
     cfg.blockDim = dim3(128);
+    PushCtx pc{};
+    if (push) pc = *push;
     return cudaLaunchKernelEx(&cfg, reduce_rows_kernel, part, part_group, lay.n_slots, B, idx_out, score_out,
-                              logZ_out, groups_out, logprob_out);
+                              logZ_out, groups_out, logprob_out, pc);
   }
   if (grp_lo && gscratch && row_ctr && B <= 64) {   // measured: B=32 14.1 -> 10.3 us; B=256 19.4 -> 24.0
     cfg.gridDim = dim3((n_groups + 7) / 8, B);
@@ -234,7 +252,7 @@ cudaError_t launch_reduce(const State* part, const int* part_group, const SlotLa
   cfg.gridDim = dim3(B);
   cfg.blockDim = dim3(kReduceThreads);
   cfg.dynamicSmemBytes = grp_lo ? 0 : (size_t)lay.n_slots * sizeof(int);
-  if (cfg.dynamicSmemBytes > 40 * 1024) {
+  if (cfg.dynamicSmemBytes > 40 * 1024) {      // per call: the size varies with the slot count
     cudaError_t e = cudaFuncSetAttribute(reduce_groups_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)cfg.dynamicSmemBytes);
     if (e != cudaSuccess) return e;
@@ -244,37 +262,34 @@ cudaError_t launch_reduce(const State* part, const int* part_group, const SlotLa
 }
 
 // ---------------------------------------------------------------------------------------------
-// Peer-memory exchange ("all-gather ... or an equivalent reduction").
-// One CTA: (1) wait until every reader consumed the previous use of this parity slot, (2) store
-// this rank's B records into slot [parity][rank] of every peer window, fence.sys, release the
-// flags, (3) acquire the n flags of this epoch in the local window, (4) outer selection over the
-// n local records per row, (5) ack the epoch into every peer window.
+// Peer-memory exchange ("all-gather ... or an equivalent reduction";
+// protocol in fs_peer.cuh).  Fused form: the shard sampler's last reduction step already pushed the
+// records and released the flags (PushCtx), so one block only (3) acquires the n flags of this
+// epoch in the local window, (4) runs the outer selection over the n local records per row, and
+// (5) acknowledges the epoch to every peer.  Unfused form (B > 256): the same block first (1)
+// waits for the readers of the parity slot and (2) pushes `local` itself.
 // ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ uint64_t globaltimer_ns() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-
-// Spin until pred(ld_acquire(p)) or ~10 s; false on timeout.
-template <typename Pred>
-__device__ __forceinline__ bool wait_flag(const uint64_t* p, Pred pred) {
-  const uint64_t t0 = globaltimer_ns();
-  uint32_t ns = 32;
-  while (!pred(ld_acquire_sys(p))) {
-    if (globaltimer_ns() - t0 > 10000000000ull) return false;
-    __nanosleep(ns);
-    ns = ns < 1024 ? ns * 2 : ns;
+__device__ __forceinline__ void wait_combine_ack(const PeerTab& peers, int world, int rank, int B, int B_max,
+                                                 uint64_t epoch, int32_t* idx_out, float* score_out,
+                                                 float* logZ_out, unsigned* timeouts, int* ok) {
+  const int par = (int)(epoch & 1);
+  if (threadIdx.x < world)
+    if (!wait_flag(peers.flags[rank] + par * world + threadIdx.x, [&](uint64_t v) { return v == epoch; })) *ok = 0;
+  __syncthreads();
+  const fs_summary* rec = peers.rec[rank] + (size_t)par * world * B_max;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    State acc = state_empty();
+    for (int k = 0; k < world; ++k) acc = state_merge(acc, from_summary(rec[(size_t)k * B_max + b]));
+    const fs_summary f = to_summary(acc);
+    idx_out[b] = *ok ? f.idx : -1;
+    if (score_out) score_out[b] = f.max_score;
+    if (logZ_out) logZ_out[b] = f.log_mass;
   }
-  return true;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (!*ok) atomicAdd(timeouts, 1u);
+    for (int p = 0; p < world; ++p) st_release_sys(peers.acks[p] + rank, epoch);
+  }
 }
 
 __global__ void __launch_bounds__(256)
@@ -298,23 +313,23 @@ exchange_combine_kernel(const fs_summary* __restrict__ local, PeerTab peers, int
     __threadfence_system();
     for (int p = 0; p < world; ++p) st_release_sys(peers.flags[p] + par * world + rank, epoch);
   }
-  if (threadIdx.x < world)
-    if (!wait_flag(peers.flags[rank] + par * world + threadIdx.x, [&](uint64_t v) { return v == epoch; })) ok = 0;
+  wait_combine_ack(peers, world, rank, B, B_max, epoch, idx_out, score_out, logZ_out, timeouts, &ok);
+}
+
+// Fused form.  Launched with PDL and never waits on the preceding grid: it synchronises with every
+// rank's pusher (including this rank's own shard kernel) through the flags alone, and triggers its
+// own dependents at once (the next step's W prefetch may start while it waits).
+__global__ void __launch_bounds__(256)
+exchange_wait_kernel(const PeerTab* __restrict__ peers_dev, int world, int rank, int B, int B_max, uint64_t epoch,
+                     int32_t* idx_out, float* score_out, float* logZ_out, unsigned* timeouts) {
+  __shared__ int ok;
+  __shared__ PeerTab peers;
+  sm100::pdl_launch_dependents();
+  if (threadIdx.x == 0) ok = 1;
+  for (int i = threadIdx.x; i < (int)(sizeof(PeerTab) / 8); i += blockDim.x)
+    reinterpret_cast<uint64_t*>(&peers)[i] = reinterpret_cast<const uint64_t*>(peers_dev)[i];
   __syncthreads();
-  const fs_summary* rec = peers.rec[rank] + (size_t)par * world * B_max;
-  for (int b = threadIdx.x; b < B; b += blockDim.x) {
-    State acc = state_empty();
-    for (int k = 0; k < world; ++k) acc = state_merge(acc, from_summary(rec[(size_t)k * B_max + b]));
-    const fs_summary f = to_summary(acc);
-    idx_out[b] = ok ? f.idx : -1;
-    if (score_out) score_out[b] = f.max_score;
-    if (logZ_out) logZ_out[b] = f.log_mass;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    if (!ok) atomicAdd(timeouts, 1u);
-    for (int p = 0; p < world; ++p) st_release_sys(peers.acks[p] + rank, epoch);
-  }
+  wait_combine_ack(peers, world, rank, B, B_max, epoch, idx_out, score_out, logZ_out, timeouts, &ok);
 }
 
 cudaError_t launch_exchange_combine(const fs_summary* local, const PeerTab& peers, int world, int rank, int B,
@@ -331,6 +346,22 @@ cudaError_t launch_exchange_combine(const fs_summary* local, const PeerTab& peer
   cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, exchange_combine_kernel, local, peers, world, rank, B, B_max, epoch, idx_out,
                             score_out, logZ_out, timeouts);
+}
+
+cudaError_t launch_exchange_wait(const PeerTab* peers_dev, int world, int rank, int B, int B_max, uint64_t epoch,
+                                 int32_t* idx_out, float* score_out, float* logZ_out, unsigned* timeouts,
+                                 cudaStream_t stream, bool pdl) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.stream = stream;
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(256);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, exchange_wait_kernel, peers_dev, world, rank, B, B_max, epoch, idx_out, score_out,
+                            logZ_out, timeouts);
 }
 
 cudaError_t launch_combine(const fs_summary* gathered, int n, int B, int32_t* idx_out, float* score_out,
@@ -366,10 +397,13 @@ cudaError_t launch_gumbel(const uint32_t* r, float* g, int64_t n, cudaStream_t s
 // overlaps this copy.
 constexpr int kCopyThreads = 256;
 constexpr int kCopyPerThread = 4;   // 16-byte words per thread per pass
+// A device-memory src may be written by the preceding kernel (PDL gives no visibility before the
+// wait), so then every load follows the wait; only a pinned host src is read early.
 __global__ void __launch_bounds__(kCopyThreads)
 copy_in_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src, int64_t n16, uint8_t* dst_tail,
-               const uint8_t* src_tail, int tail) {
+               const uint8_t* src_tail, int tail, int src_host) {
   sm100::pdl_launch_dependents();
+  if (!src_host) sm100::pdl_wait();
   const int64_t stride = (int64_t)gridDim.x * kCopyThreads;
   int64_t i0 = (int64_t)blockIdx.x * kCopyThreads + threadIdx.x;
   uint4 v[kCopyPerThread];
@@ -386,7 +420,7 @@ copy_in_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src, int64_t n
   for (int64_t i = i0 + kCopyPerThread * stride; i < n16; i += stride) dst[i] = src[i];
 }
 
-cudaError_t launch_copy_in(void* dst, const void* src, size_t bytes, bool pdl, cudaStream_t stream) {
+cudaError_t launch_copy_in(void* dst, const void* src, size_t bytes, bool pdl, bool src_host, cudaStream_t stream) {
   const int64_t n16 = (int64_t)(bytes / 16);
   const int tail = (int)(bytes % 16);
   const int64_t per_block = (int64_t)kCopyThreads * kCopyPerThread;
@@ -401,7 +435,8 @@ cudaError_t launch_copy_in(void* dst, const void* src, size_t bytes, bool pdl, c
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, copy_in_kernel, static_cast<uint4*>(dst), static_cast<const uint4*>(src), n16,
-                            static_cast<uint8_t*>(dst) + n16 * 16, static_cast<const uint8_t*>(src) + n16 * 16, tail);
+                            static_cast<uint8_t*>(dst) + n16 * 16, static_cast<const uint8_t*>(src) + n16 * 16, tail,
+                            src_host ? 1 : 0);
 }
 
 }  // namespace fs

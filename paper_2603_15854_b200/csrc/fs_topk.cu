@@ -702,13 +702,10 @@ cudaError_t launch_topk_final(const Cand* cand, int ncand, int* row_count, int B
   // survivors are staged in shared memory next to the static arrays (~38 KB)
   constexpr int kDynMax = 180 * 1024;
   const int smem_cand = kDynMax / (int)sizeof(Cand);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(topk_final_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynMax);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(topk_final_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynMax);
+  {
+    cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(topk_final_kernel<true>), kDynMax);
+    if (e == cudaSuccess) e = ensure_smem_attr(reinterpret_cast<const void*>(topk_final_kernel<false>), kDynMax);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.stream = stream;

@@ -55,3 +55,19 @@ def test_host_validation_without_gpu():
 def test_version_string():
     import paper_2603_15854_b200 as fs
     assert "sm_100a" in fs.version()
+
+
+def test_tp_entry_points_host_side():
+    """§8(b) TP boundary without a GPU: NCCL is resolved at run time (a fresh unique id comes back),
+    NULL arguments are rejected, and fs_sample_tp refuses a context without a communicator."""
+    from paper_2603_15854_b200 import _lib
+    L = _lib.lib()
+    assert L.fs_status_str(_lib.FS_ERR_NCCL) == b"FS_ERR_NCCL"
+    assert L.fs_comm_init(None, None, 1, 0) == _lib.FS_ERR_INVALID
+    assert L.fs_comm_unique_id(None) == _lib.FS_ERR_INVALID
+    a, b = ctypes.create_string_buffer(128), ctypes.create_string_buffer(128)
+    assert L.fs_comm_unique_id(a) == _lib.FS_OK, L.fs_last_error()
+    assert L.fs_comm_unique_id(b) == _lib.FS_OK
+    assert a.raw != b"\0" * 128 and a.raw != b.raw
+    st = L.fs_sample_tp(None, 0, None, None, None, None, None, 0, 0, 1, 1, 1, 0, 1, None, None, None, None, None)
+    assert st == _lib.FS_ERR_INVALID

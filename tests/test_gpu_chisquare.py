@@ -57,3 +57,28 @@ def test_fused_sampler_chi_square_1e6(variant):
         if p > 1e-3:
             break
     assert p > 1e-3, (counts, p)
+
+
+def test_tiny_config_fp32_chi_square_1e6_every_row():
+    """BASELINE.json configs[0] (B=4, D=64, V=1000 fp32, CUDA-core fp32 kernel): >= 1e6 draws per
+    row vs softmax(l~) of the oracle's fp64 logits, p > 0.001.  The 4 rows are replicated 64 times
+    (batch row b = r + 4j); distinct b draw independent Gumbels, so one launch gives 64 draws of
+    each row; 15625 steps -> 1,000,000 draws per row."""
+    from oracle import sampler
+    wl = synth.make_workload("tiny", 4)
+    lt = sampler.scores(synth.as_numpy_exact(wl.h), synth.as_numpy_exact(wl.W), seed=wl.seed, step=0).ltilde
+    h = wl.h.repeat(64, 1).cuda().contiguous()
+    W = wl.W.cuda()
+    out = torch.empty(256, dtype=torch.int32, device="cuda")
+    for seed in (wl.seed, 20260303):
+        counts = torch.zeros(4, 1000, dtype=torch.int64, device="cuda")
+        rows = torch.arange(256, device="cuda") % 4
+        for s in range(15625):
+            fs.sample(h, W, seed=seed, step=s, out=out)
+            counts.index_put_((rows, out.long()), torch.ones(256, dtype=torch.int64, device="cuda"), accumulate=True)
+        counts = counts.cpu().numpy()
+        assert (counts.sum(axis=1) == 1_000_000).all()
+        ps = [stats.chi_square(counts[r], stats.softmax_probs(lt[r]))[1] for r in range(4)]
+        if min(ps) > 1e-3:
+            break
+    assert min(ps) > 1e-3, ps

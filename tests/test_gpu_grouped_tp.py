@@ -139,3 +139,32 @@ def test_grouped_and_tp_on_cta_pairs(pair_on):
                              mask=mask, seed=wl.seed, step=2).raw for a, b in sampler.shard_bounds(wl.V, 4)]
     tidx, tscore, _ = fs.combine_summaries(torch.stack(parts), return_all=True)
     assert torch.equal(tidx, fidx) and torch.equal(tscore, fscore)
+
+
+@pytest.fixture
+def grp_ranges_reset():
+    yield
+    fs.set_option("grp_ranges", 1)
+
+
+@pytest.mark.parametrize("B", [65, 128, 256])
+@pytest.mark.parametrize("ranges", [1, 0])
+def test_grouped_large_batch_stage2_vs_oracle(B, ranges, grp_ranges_reset):
+    """B > 64 takes the block-per-row stage 2 (reduce_groups_kernel, host slot ranges or the device
+    binary search); every row, every group against the oracle (O7, §4.1)."""
+    fs.set_option("grp_ranges", ranges)
+    wl = synth.make_workload("gemma3_27b", B, V=9000 + 64, D=128, with_transforms=True)
+    h, W, bias, tau, mask = (x.cuda() for x in (wl.h, wl.W, wl.bias, wl.temperature, wl.mask))
+    idx, score, logZ, groups, logprob = fs.sample_grouped(h, W, group_size=1024, bias=bias, temperature=tau,
+                                                          mask=mask, seed=wl.seed, step=4, return_logprob=True)
+    fidx, fscore = fs.sample(h, W, bias=bias, temperature=tau, mask=mask, seed=wl.seed, step=4, return_score=True)
+    torch.cuda.synchronize()
+    assert torch.equal(idx, fidx) and torch.equal(score.view(torch.int32), fscore.view(torch.int32))
+    sc, flat = oracle_flat(wl, 4)
+    check_flat(idx.cpu().numpy(), score.cpu().numpy(), flat)
+    fin = np.isfinite(flat.logZ)
+    assert np.all(np.abs(logZ.cpu().numpy()[fin] - flat.logZ[fin]) <= LOGMASS_TOL)
+    lp_ref = sampler.log_prob(sc, flat)
+    same = idx.cpu().numpy() == flat.idx
+    assert np.all(np.abs(logprob.cpu().numpy()[same] - lp_ref[same]) <= LOGMASS_TOL + SCORE_TOL)
+    _groups_vs_oracle(groups, sc, 1024)

@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 if torch.cuda.is_available():
     import paper_2603_15854_b200 as fs
 
-OPTS = (("fuse_reduce", 1), ("pdl_w", 0), ("pdl", 1), ("pair", -1), ("max_ctas", 0))
+OPTS = (("fuse_reduce", 1), ("pdl_w", 0), ("pdl", 1), ("pair", -1), ("max_ctas", 0), ("staging_check", 1))
 
 
 @pytest.fixture(autouse=True)
@@ -267,3 +267,70 @@ def test_grouped_host_slot_ranges_equal_device_search(opts, V, g, B):
     assert torch.equal(g0[..., :2], g1[..., :2])                       # max_score, idx
     torch.testing.assert_close(g0[..., 2].view(torch.float32), g1[..., 2].view(torch.float32), rtol=1e-6,
                                atol=1e-6)
+
+
+@pytest.mark.parametrize("B", [8, 64])
+def test_staged_grid_too_large_falls_back_to_copy_kernel(B):
+    # in-kernel staging needs every CTA co-resident.  A persistent grid larger than the
+    # device (max_ctas > #SMs) must be staged by the copy kernel instead -- same ids, counted.
+    wl = synth.make_workload("llama3_8b", B, V=60000, D=256, seed_offset=3)
+    W = wl.W.cuda()
+    h_host = wl.h.pin_memory()
+    h_dev = torch.empty(h_host.shape, dtype=h_host.dtype, device="cuda")
+    out = torch.full((B,), -7, dtype=torch.int32).pin_memory()
+    n_sms = int(fs.query("num_sms"))
+    fs.set_option("max_ctas", 2 * n_sms + 2)
+    before = fs.query("staged_fallbacks")
+    fs.sample_from_host(h_host, W, seed=wl.seed, step=3, h_dev=h_dev, idx_host=out)
+    torch.cuda.synchronize()
+    assert fs.query("staged_fallbacks") == before + 1
+    ref = fs.sample(wl.h.cuda(), W, seed=wl.seed, step=3)
+    assert torch.equal(ref.cpu(), out)
+
+
+def test_staging_barrier_timeout_is_recoverable():
+    # Forced in-kernel staging with a grid that cannot be co-resident: the resident CTAs give up the
+    # grid barrier after ~5 s instead of trapping; the call completes with every row undefined
+    # (idx -1), the event is counted, and the context keeps working (no sticky CUDA error).
+    B = 4
+    wl = synth.make_workload("llama3_8b", B, V=80000, D=128, seed_offset=4)
+    W = wl.W.cuda()
+    h_host = wl.h.pin_memory()
+    h_dev = torch.empty(h_host.shape, dtype=h_host.dtype, device="cuda")
+    out = torch.full((B,), -7, dtype=torch.int32).pin_memory()
+    n_sms = int(fs.query("num_sms"))
+    fs.set_option("max_ctas", 3 * n_sms)
+    fs.set_option("staging_check", 0)
+    before = fs.query("staging_timeouts")
+    fs.sample_from_host(h_host, W, seed=wl.seed, step=1, h_dev=h_dev, idx_host=out)
+    torch.cuda.synchronize()
+    assert fs.query("staging_timeouts") == before + 1
+    assert bool((out == -1).all())
+    fs.set_option("staging_check", 1)
+    fs.set_option("max_ctas", 0)
+    fs.sample_from_host(h_host, W, seed=wl.seed, step=1, h_dev=h_dev, idx_host=out)
+    torch.cuda.synchronize()
+    ref = fs.sample(wl.h.cuda(), W, seed=wl.seed, step=1)
+    assert torch.equal(ref.cpu(), out)
+
+
+def test_contexts_per_stream_sample_concurrently():
+    # the binding keys contexts by (device, stream), so two streams sampling at once use
+    # separate workspaces; results equal the serial calls bit for bit.
+    wl = synth.make_workload("qwen25_7b", 48, V=30000, D=256, seed_offset=9)
+    g = _gpu(wl)
+    serial = [_sample(g, wl, s) for s in (1, 2)]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = []
+    torch.cuda.synchronize()
+    for rep in range(3):
+        res = []
+        for s, st in zip((1, 2), streams):
+            with torch.cuda.stream(st):
+                res.append(fs.sample(g["h"], g["W"], bias=g["bias"], temperature=g["temperature"], mask=g["mask"],
+                                     seed=wl.seed, step=s, return_score=True))
+        outs.append(res)
+    torch.cuda.synchronize()
+    for res in outs:
+        for (i, sc), (ri, rs) in zip(res, serial):
+            assert np.array_equal(i.cpu().numpy(), ri) and np.array_equal(sc.cpu().numpy(), rs)

@@ -66,6 +66,8 @@ def _check(idx, score, res):
         if res.gap[r] > 1e-2:
             assert idx[r] == res.idx[r], (r, idx[r], res.idx[r])
             exact += 1
+        else:                                             # near tie: one of the near-tied kept ids
+            assert int(idx[r]) in res.near[r], (r, idx[r], res.near[r])
     return exact, decisive
 
 

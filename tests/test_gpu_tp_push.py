@@ -9,6 +9,8 @@ both parity slots and the reader acknowledgements are exercised."""
 import os
 import socket
 
+import numpy as np
+
 import pytest
 import torch
 import torch.distributed as dist
@@ -31,6 +33,8 @@ def _worker(rank, world, port, cfg, B, V, D, steps, q):
         os.environ["MASTER_PORT"] = str(port)
         dist.init_process_group("gloo", rank=rank, world_size=world)
         torch.cuda.set_device(0)
+        import sys
+        sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
         import synth
         import paper_2603_15854_b200 as fs
         from paper_2603_15854_b200 import tp
@@ -42,6 +46,7 @@ def _worker(rank, world, port, cfg, B, V, D, steps, q):
         mask = None if wl.mask is None else wl.mask.to(dev)
         lo, hi = tp.shard_bounds(V, world, rank)
         tp.PushExchange(B_max=B)
+        from parity import check_flat, oracle_flat
         out = []
         for s in range(steps):
             idx, score, logZ = tp.sample_tp_push_step(
@@ -49,8 +54,14 @@ def _worker(rank, world, port, cfg, B, V, D, steps, q):
                 temperature=tau, mask=mask, seed=wl.seed, step=s, return_all=True)
             ref_idx, ref_score = fs.sample(h, W, bias=bias, temperature=tau, mask=mask, seed=wl.seed, step=s,
                                            return_score=True)
+            oracle_ok = True
+            if s in (0, steps - 1):          # the exchanged result against the fp64 oracle (every row)
+                _, flat = oracle_flat(wl, s)
+                check_flat(idx.cpu().numpy(), score.cpu().numpy(), flat)
+                fin = np.isfinite(flat.logZ)
+                oracle_ok = bool(np.all(np.abs(logZ.cpu().numpy()[fin] - flat.logZ[fin]) <= 1e-3))
             out.append((torch.equal(idx, ref_idx), torch.equal(score.view(torch.int32), ref_score.view(torch.int32)),
-                        bool(torch.isfinite(logZ).all())))
+                        oracle_ok))
         timeouts = fs.query("comm_timeouts")
         dist.barrier()                       # peers stay mapped until everyone is done
         fs.comm_window_destroy()
@@ -60,8 +71,9 @@ def _worker(rank, world, port, cfg, B, V, D, steps, q):
         q.put((rank, None, None, repr(e)))
 
 
+# B <= 16: the last stage-1 CTA pushes; 17..256: the stage-2 row reduce pushes; > 256: separate push kernel
 @pytest.mark.parametrize("world,cfg,B,V,D", [(2, "llama3_8b", 8, 20011, 256), (3, "qwen25_7b", 33, 9001, 128),
-                                             (4, "llama3_8b", 1, 4096, 64)])
+                                             (4, "llama3_8b", 1, 4096, 64), (2, "qwen25_7b", 300, 5003, 64)])
 def test_push_exchange_matches_single_gpu(world, cfg, B, V, D):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -76,3 +88,28 @@ def test_push_exchange_matches_single_gpu(world, cfg, B, V, D):
         assert err is None, (rank, err)
         assert timeouts == 0
         assert all(a and b and c for a, b, c in out), (rank, out)
+
+
+def test_nccl_sample_tp_world1_equals_single_gpu():
+    """fs_comm_init + fs_sample_tp (library NCCL, §8(b)) on a one-rank communicator: the whole
+    shard -> ncclAllGather -> combine sequence runs on the device and equals fs_sample / the oracle."""
+    import paper_2603_15854_b200 as fs
+    import synth
+    from parity import check_flat, oracle_flat
+    torch.cuda.set_device(0)
+    fs.comm_init(fs.comm_unique_id(), 1, 0)
+    wl = synth.make_workload("qwen25_7b", 40, V=7001, D=128)
+    dev = {k: getattr(wl, k).cuda() for k in ("h", "W", "bias", "temperature", "mask")}
+    for step in range(3):
+        idx, score, logZ, ranks = fs.sample_tp(dev["h"], dev["W"], 0, wl.V, bias_shard=dev["bias"],
+                                               temperature=dev["temperature"], mask=dev["mask"], seed=wl.seed,
+                                               step=step, return_all=True, per_rank=True)
+        ref_idx, ref_score = fs.sample(dev["h"], dev["W"], bias=dev["bias"], temperature=dev["temperature"],
+                                       mask=dev["mask"], seed=wl.seed, step=step, return_score=True)
+        torch.cuda.synchronize()
+        assert torch.equal(idx, ref_idx)
+        assert torch.equal(score.view(torch.int32), ref_score.view(torch.int32))
+        assert torch.equal(ranks.idx[0], idx)
+    _, flat = oracle_flat(wl, 2)
+    check_flat(idx.cpu().numpy(), score.cpu().numpy(), flat)
+    fs.comm_destroy()

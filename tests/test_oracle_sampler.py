@@ -316,6 +316,7 @@ def test_topk_topp_special_cases_and_hand_example():
     flat = sampler.flat_sample(sc)
     full = sampler.topk_topp_sample(sc, top_k=200, top_p=1.0)       # no truncation == flat
     assert np.array_equal(full.idx, flat.idx) and np.array_equal(full.s1, flat.s1)
+    assert full.near == [sorted(x) for x in flat.near]               # same near-tie sets
     one = sampler.topk_topp_sample(sc, top_k=1)                      # k = 1 == greedy argmax of l~
     assert np.array_equal(one.idx, np.argmax(sc.ltilde, axis=1))
     # hand example: l~ = ln[1,2,3,4]; k=4, p=0.5: sorted q = [.4,.3,.2,.1], cumsum .4,.7 -> keep {3,2}

@@ -51,7 +51,10 @@ def _worker(rank, world, port, result_q):
     idx, best, logZ = sampler.combine_shard_summaries(M, I, L)
     flat = sampler.flat_sample(sampler.scores(a["h"], a["W"], seed=wl.seed, step=4, bias=a["bias"],
                                               temperature=a["temperature"], mask=a["mask"]))
-    result_q.put((rank, idx.tolist(), flat.idx.tolist(), float(np.max(np.abs(logZ - flat.logZ)))))
+    # NcclComm's host plumbing: rank 0's NCCL unique id reaches every rank unchanged (fs_comm_init
+    # itself needs a GPU per rank)
+    uid = tp.broadcast_unique_id()
+    result_q.put((rank, idx.tolist(), flat.idx.tolist(), float(np.max(np.abs(logZ - flat.logZ))), uid))
     dist.destroy_process_group()
 
 
@@ -66,7 +69,9 @@ def test_tp_exchange_world2_gloo():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for rank, idx, flat_idx, lz_err in res:
+    for rank, idx, flat_idx, lz_err, uid in res:
         assert idx == flat_idx
         assert lz_err < 1e-5          # fp32-rounded summaries
+        assert len(uid) == 128
     assert res[0][1] == res[1][1]
+    assert res[0][4] == res[1][4]

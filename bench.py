@@ -4,19 +4,27 @@
     python bench.py [--gpus N --steps K --warmup W] [--config llama3_8b] [--B 32] [--impl reference]
 
 Metric (BASELINE.json): "LM-head+sample us/step & HBM GB/s vs peak, B=1-256, V=128K-262K".
-A step = one pass of the whole hot path (stage-1 fused kernel + stage-2 reduce; for N>1 also
-the summary all-gather and combine) over one batch of synthetic decode hidden states.
+A step = one pass of the whole hot path (the fused stage-1 kernel, whose last
+CTA also runs stage 2 for plain sampling; for N>1 also the B x 12-byte summary all-gather and the
+combine, a8) over one batch of synthetic decode hidden states.
 
 N=1 : workload = BASELINE.json configs[1], Llama-3-8B LM head (D=4096, V=128256, bf16), B=32
-      (the north-star "B<=32" target).  The JSON line also carries the B in {1,8,32,128,256}
-      sweep with the unfused baselines measured on the same box.
-N>1 : (torchrun, one rank per GPU, NCCL) the same workload vocabulary-sharded (Alg. A.4):
-      every rank streams V/N rows and the ranks all-gather B x 12-byte summaries.
-      scaling = "strong" (total work fixed).
+      (the north-star "B<=32" target).  `value` = K back-to-back steps with NO cross-step overlap
+      (pdl_w=0: every step's kernel starts after the previous one finished) -- the honest step
+      latency.  The PDL-pipelined period (next step's W stream starting under the previous step's
+      tail) is reported separately as `pipelined_us`, the paper's per-call median as
+      `per_call_median_us`.  The JSON line also carries the B in {1,8,32,128,256} sweep of every
+      BASELINE.json config (+ the paper's own D=4096, V=151936 workload) with the unfused
+      baselines measured on the same box, the per-rank compute of the vocab-sharded 70B step at
+      n=2/4/8, and the CPU oracle timed with 1 thread and with every host core.
+N>1 : (torchrun, one rank per GPU, NCCL) the same workload vocabulary-sharded (Alg. A.4): every
+      rank streams V/N rows and the library all-gathers B x 12-byte summaries (fs_sample_tp,
+      its own NCCL communicator).  scaling = "strong" (total work fixed).
 --impl reference : the fp64 CPU oracle (oracle/), timed on the host cores on a bounded
-      vocabulary sample of the same workload, scaled to a full step.
+      vocabulary sample of the same workload, scaled to a full step; same config dict.
 
-W (1.05 GB) is larger than L2 (126 MB), so successive steps stream it from HBM; no flush.
+W (>= 1.05 GB) is larger than L2 (126 MB), so successive steps stream it from HBM; no flush
+(the 70B n=8 shard, 263 MB, is also > 2x L2).
 """
 from __future__ import annotations
 
@@ -39,6 +47,13 @@ import synth  # noqa: E402
 
 METRIC = "LM-head+sample µs/step & HBM GB/s vs peak, B=1–256, V=128K–262K"
 UNIT = "us/step"
+SWEEP_B = (1, 8, 32, 128, 256)
+PAPER_B = (1, 8, 32, 64, 128, 256)
+# PAPER.md Table 3, B200 column: FlashSampling speedup vs Multinomial (compiled) / FI1 / FI2
+# at D=4096, V=151936 -- context for the "paper_d4096" sweep (another implementation, same GPU type).
+PAPER_TABLE3_B200 = {1: (1.46, 1.51, 1.32), 2: (1.46, 1.56, 1.30), 4: (1.47, 1.61, 1.32), 8: (1.53, 1.61, 1.33),
+                     16: (1.57, 1.65, 1.36), 32: (1.68, 1.68, 1.38), 64: (1.84, 1.67, 1.39),
+                     128: (1.89, 1.55, 1.27), 256: (1.58, 1.32, 1.07)}
 
 
 # ----------------------------------------------------------------------------------------------
@@ -52,8 +67,8 @@ def peaks():
 
 
 def algorithmic_bytes(B, D, V, transforms=False, n_groups=0, tp_world=1):
-    """Bytes the method must move per step: W once, h, transforms,
-    outputs; the [B,V] logits are never materialised.  Candidate scratch is excluded."""
+    """Bytes the method must move per step: W once, h, transforms, outputs; the
+    [B,V] logits are never materialised.  Candidate scratch is excluded."""
     b = 2 * V * D + 2 * B * D + 4 * B
     if transforms:
         b += 4 * V + 4 * B + 4 * B * ((V + 31) // 32)
@@ -71,9 +86,26 @@ def stage1_bytes(B, D, V, transforms=False):
     return b
 
 
+def config_dict(name, B, world=1):
+    """The workload description both arms print (identical dicts for the same workload)."""
+    cfg = synth.CONFIGS[name]
+    D, V = cfg["D"], cfg["V"]
+    desc = f"{name} LM head, B={B}"
+    if cfg.get("group_size"):
+        desc += f", grouped g={cfg['group_size']} ({(V + cfg['group_size'] - 1) // cfg['group_size']} groups)"
+    if "temperature" in cfg:
+        desc += f", tau={cfg['temperature']} + bias + {int(100 * cfg['mask_ban_frac'])}% mask"
+    if world > 1:
+        desc += ", vocab-sharded TP (Alg. A.4)"
+    return {"workload": desc, "B": B, "D": D, "V": V,
+            "parallelism": "single GPU" if world == 1 else f"tp{world} (vocab)",
+            "l2": "no flush: W (%.2f GB%s) > L2 (126 MB), re-streamed from HBM every step"
+                  % (2 * V * D / max(1, world) / 1e9, " per rank" if world > 1 else "")}
+
+
 class ClockSampler:
     """SM clock / power / clock-event reasons sampled while running: NVML polled every 5 ms from a
-    thread (enough samples inside a sub-second timed region); nvidia-smi every 100 ms as fallback."""
+    thread; nvidia-smi every 100 ms as fallback."""
     FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
               "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
               "clocks_event_reasons.sw_power_cap"]
@@ -108,6 +140,7 @@ class ClockSampler:
 
     def __enter__(self):
         self.stop = False
+        self.t_start = time.time()
         try:
             import pynvml as nv
             nv.nvmlInit()
@@ -139,6 +172,7 @@ class ClockSampler:
 
     def __exit__(self, *a):
         self.stop = True
+        self.t_end = time.time()
         if getattr(self, "source", "") == "nvml":
             self.thread.join(timeout=1)
         if self.proc:
@@ -149,16 +183,18 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        win = round(1e3 * (getattr(self, "t_end", time.time()) - getattr(self, "t_start", time.time())), 1)
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "window_ms": win}
         sm = [float(p[0]) for _, p in self.samples if p[0].replace(".", "").isdigit()]
         mx = [float(p[1]) for _, p in self.samples if p[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for _, p in self.samples for i in range(4) if p[3 + i].lower() == "active"})
+        counts = {names[i]: sum(1 for _, p in self.samples if p[3 + i].lower() == "active") for i in range(4)}
         pw = [float(p[2]) for _, p in self.samples if p[2].replace(".", "").isdigit()]
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples), "power_w_median": statistics.median(pw) if pw else None,
-                "source": getattr(self, "source", None)}
+                "reasons": sorted(k for k, v in counts.items() if v), "reason_samples": {k: v for k, v in counts.items() if v},
+                "samples": len(self.samples), "window_ms": win,
+                "power_w_median": statistics.median(pw) if pw else None, "source": getattr(self, "source", None)}
 
 
 def time_loop(fn, steps, warmup, stream=None):
@@ -178,7 +214,7 @@ def time_loop(fn, steps, warmup, stream=None):
 
 
 def time_median(fn, iters, warmup):
-    """Median of per-call event times (the paper's protocol: 25 warm-ups, median of 100)."""
+    """Median of per-call event times (the paper's protocol: 25 warm-ups, median of 100, P:474/498)."""
     for _ in range(warmup):
         fn()
     torch.cuda.synchronize()
@@ -189,6 +225,38 @@ def time_median(fn, iters, warmup):
         b.record()
     torch.cuda.synchronize()
     return statistics.median(a.elapsed_time(b) for a, b in evs)
+
+
+def timed_region(fn, steps, warmup, device_index=0, clock_window_s=0.12, barrier=None):
+    """The contract's timed region: W warm-ups, then a pre-roll of the same step long enough that the
+    clock sampler sees >= clock_window_s of this load, then sync (+ barrier), exactly K steps between
+    CUDA events on the launching stream, sync (+ barrier).  Returns (ms per step, clocks summary)."""
+    stream = torch.cuda.current_stream()
+    for _ in range(max(3, warmup)):
+        fn()
+    torch.cuda.synchronize()
+    est = time_loop(fn, 10, 0)
+    n_pre = max(0, int(math.ceil(clock_window_s / max(1e-6, est * 1e-3))) - steps)
+    with ClockSampler(device_index) as clk:
+        for _ in range(n_pre):
+            fn()
+        torch.cuda.synchronize()
+        if barrier:
+            barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if barrier:
+            barrier()
+        torch.cuda.synchronize()
+    c = clk.summary()
+    c["preroll_steps"] = n_pre
+    return e0.elapsed_time(e1) / steps, c
 
 
 # ----------------------------------------------------------------------------------------------
@@ -223,25 +291,42 @@ def fused_step_fn(fs, wl, step_ctr, out):
     return fn
 
 
-def baselines(wl, iters, warmup):
+_COMPILED = {}
+
+
+def _multinomial_fn(transforms, groups_g, V):
+    """GEMM -> fp32 -> (+bias)/tau -> masked_fill -> softmax -> torch.multinomial, plus the
+    log-normaliser and per-group log-masses when the workload is the grouped one."""
+    def f(h, W, bias, tau, allowed):
+        lg = torch.matmul(h, W.t()).float()
+        if transforms:
+            lg = ((lg + bias) / tau[:, None]).masked_fill(~allowed, float("-inf"))
+        out = torch.multinomial(torch.softmax(lg, -1), 1)
+        if groups_g:
+            pad = (-V) % groups_g
+            lgp = torch.nn.functional.pad(lg, (0, pad), value=float("-inf"))
+            return out, torch.logsumexp(lgp.view(lg.shape[0], -1, groups_g), dim=-1), torch.logsumexp(lg, dim=-1)
+        return out
+    return f
+
+
+def baselines(name, wl, iters, warmup, compiled=True):
     """Unfused paths on the same inputs: cuBLAS GEMM alone; GEMM + softmax +
-    torch.multinomial (eager); FlashInfer FI2 (Gumbel-max on logits) and FI1 (top-k/top-p).
-    For the grouped workload the unfused path must also produce the log-normalizer and the
-    per-group log-masses (torch.logsumexp over the materialised logits)."""
+    torch.multinomial, eager and torch.compile'd (the paper's "Multinomial"); FlashInfer FI2
+    (Gumbel-max on logits) and FI1 (top-k 50 / top-p 0.95, reading R17).  For the grouped workload the
+    unfused path must also produce the log-normaliser and the per-group log-masses.  The vocabulary
+    mask is handed to the baselines already unpacked to bool (their most favourable input form)."""
     h, W, bias, tau, mask = wl["h"], wl["W"], wl["bias"], wl["temperature"], wl["mask"]
     V = W.shape[0]
     g = wl["group_size"]
+    transforms = bias is not None
+    allowed = synth.unpack_allowed_bits(mask, V) if mask is not None else None
     res = {}
 
     def transformed():
         lg = torch.matmul(h, W.t()).float()
-        if bias is not None:
-            lg = lg + bias
-        if tau is not None:
-            lg = lg / tau[:, None]
-        if mask is not None:
-            allowed = synth.unpack_allowed_bits(mask, V)
-            lg = lg.masked_fill(~allowed, float("-inf"))
+        if transforms:
+            lg = ((lg + bias) / tau[:, None]).masked_fill(~allowed, float("-inf"))
         return lg
 
     def with_groups(sampler_fn):
@@ -257,8 +342,21 @@ def baselines(wl, iters, warmup):
         return fn
 
     res["cublas_gemm_only_us"] = 1e3 * time_median(lambda: torch.matmul(h, W.t()), iters, warmup)
-    res["gemm_softmax_multinomial_eager_us"] = 1e3 * time_median(
-        with_groups(lambda lg: torch.multinomial(torch.softmax(lg, -1), 1)), iters, warmup)
+    mfn = _multinomial_fn(transforms, g, V)
+    res["multinomial_eager_us"] = 1e3 * time_median(lambda: mfn(h, W, bias, tau, allowed), iters, warmup)
+    if compiled:
+        try:
+            key = (name, transforms, g)
+            if key not in _COMPILED:
+                _COMPILED[key] = torch.compile(mfn, dynamic=True)
+            cf = _COMPILED[key]
+            t0 = time.time()
+            cf(h, W, bias, tau, allowed)
+            torch.cuda.synchronize()
+            res["multinomial_compiled_us"] = 1e3 * time_median(lambda: cf(h, W, bias, tau, allowed), iters, warmup)
+            res["multinomial_compile_s"] = round(time.time() - t0, 1)
+        except Exception as e:  # pragma: no cover - inductor unavailable on the box
+            res["multinomial_compiled_error"] = repr(e)[:200]
     try:
         import flashinfer.sampling as fis
         res["fi2_gemm_sampling_from_logits_us"] = 1e3 * time_median(
@@ -271,35 +369,56 @@ def baselines(wl, iters, warmup):
 
 
 # ----------------------------------------------------------------------------------------------
-def cpu_oracle_step_us(name, B, seconds, with_tp_world=1):
-    """Time the fp64 oracle (as it stands) on a bounded vocabulary slice of the workload and
-    scale to a full step.  Returns (us_per_full_step, cores, sample description)."""
-    import numpy as np
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def cpu_oracle_step_us(name, B, seconds, threads=None):
+    """Time the fp64 oracle (as it stands) on a bounded vocabulary slice of the workload and scale
+    to a full step.  threads=1 pins numpy's BLAS pool to one thread; None leaves every host core.
+    Returns (us_per_full_step, threads used, sample description)."""
     from oracle import sampler
     try:
-        from threadpoolctl import threadpool_info
-        cores = max([d.get("num_threads", 1) for d in threadpool_info()] + [1])
-    except Exception:
-        cores = os.cpu_count()
+        from threadpoolctl import threadpool_limits
+    except Exception:  # pragma: no cover
+        threadpool_limits = None
     cfg = synth.CONFIGS[name]
     D, V = cfg["D"], cfg["V"]
     Vs = 4096
     wl = synth.make_workload(name, B, V=Vs, D=D)
     a = dict(h=synth.as_numpy_exact(wl.h), W=synth.as_numpy_exact(wl.W), bias=synth.as_numpy_exact(wl.bias),
              temperature=synth.as_numpy_exact(wl.temperature), mask=synth.as_numpy_exact(wl.mask))
-    t0 = time.perf_counter()
-    n = 0
-    while True:
-        sc = sampler.scores(a["h"], a["W"], seed=synth.SAMPLING_SEED, step=n, bias=a["bias"],
-                            temperature=a["temperature"], mask=a["mask"])
-        sampler.flat_sample(sc, want_near=False)
-        n += 1
-        el = time.perf_counter() - t0
-        if el >= seconds:
-            break
+    nthreads = 1 if threads == 1 else host_cores()
+    ctxm = threadpool_limits(limits=nthreads) if threadpool_limits else None
+    if ctxm:
+        ctxm.__enter__()
+    try:
+        t0 = time.perf_counter()
+        n = 0
+        while True:
+            sc = sampler.scores(a["h"], a["W"], seed=synth.SAMPLING_SEED, step=n, bias=a["bias"],
+                                temperature=a["temperature"], mask=a["mask"])
+            sampler.flat_sample(sc, want_near=False)
+            n += 1
+            el = time.perf_counter() - t0
+            if el >= seconds:
+                break
+    finally:
+        if ctxm:
+            ctxm.__exit__(None, None, None)
     per_slice = el / n
-    return 1e6 * per_slice * (V / Vs), cores, (f"{n} oracle passes over a {Vs}-row vocabulary slice "
-                                              f"(all {B} rows, D={D}); scaled x{V / Vs:.2f} to V={V}")
+    return 1e6 * per_slice * (V / Vs), nthreads, (f"{n} oracle passes over a {Vs}-row vocabulary slice "
+                                                  f"(all {B} rows, D={D}) in {el:.1f} s; scaled x{V / Vs:.2f} to V={V}")
+
+
+def cpu_baseline(name, B, seconds):
+    us_all, cores, sample = cpu_oracle_step_us(name, B, seconds)
+    us_one, _, sample_one = cpu_oracle_step_us(name, B, seconds, threads=1)
+    return {"value": round(us_all, 1), "unit": UNIT, "cores": cores, "nproc": host_cores(), "kind": "oracle",
+            "sample": sample, "one_thread": {"value": round(us_one, 1), "unit": UNIT, "cores": 1, "sample": sample_one}}
 
 
 def run_reference(args):
@@ -314,10 +433,10 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": round(us, 1), "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(us / 1e3, 3),
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded, BASELINE.json shapes)",
-            "config": {"workload": f"{name} LM head, B={B}", "B": B, "D": synth.CONFIGS[name]["D"],
-                       "V": synth.CONFIGS[name]["V"]},
-            "cpu_baseline": {"value": round(us, 1), "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "data": "synthetic (seeded h~N(0,1), W~N(0,0.02^2), bf16; random-init LM head)",
+            "config": config_dict(name, B, args.gpus),
+            "cpu_baseline": {"value": round(us, 1), "unit": UNIT, "cores": cores, "nproc": host_cores(),
+                             "kind": "oracle", "sample": sample},
             "e2e": {"value": round(us, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -333,26 +452,42 @@ def load_traffic(name, B):
         return None
 
 
-def roofline(name, B, D, V, t_stage1_ms, pk, transforms):
+def roofline(name, B, D, V, t_kernel_ms, pk, transforms, kname=None, traffic_key=None):
+    """Roofline of the stage-1 kernel: algorithmic bytes and 2BVD flops over the
+    kernel's measured launch time.  The bound is the larger of t_HBM (measured copy peak) and t_TC at
+    the SUSTAINED bf16 rate (the kernel is timed inside a long loop, MEASURED_PEAKS.json)."""
     byts = stage1_bytes(B, D, V, transforms)
     flops = 2.0 * B * V * D
     t_hbm = byts / (pk["hbm_gbs"] * 1e9)
-    t_tc = flops / (pk["bf16_tflops"] * 1e12)
-    t = t_stage1_ms * 1e-3
-    traffic = load_traffic(name, B)
-    # the library picks the CTA-pair kernel from MMA N >= 32 (B > 16), else the 1-CTA kernel
-    kname = "fused_tc2_kernel (CTA pair, stage 1)" if B > 16 else "fused_tc_kernel (stage 1)"
+    t_tc = flops / (pk["bf16_tflops_sustained"] * 1e12)
+    t = t_kernel_ms * 1e-3
+    traffic = load_traffic(*(traffic_key or (name, B)))
+    kname = kname or ("fused_tc2_kernel (CTA pair, stage 1)" if B > 16 else "fused_tc_kernel (stage 1)")
+    common = {"traffic": traffic, "kernel": kname, "kernel_us": round(t * 1e6, 2), "algorithmic_bytes": byts,
+              "flops": flops, "peak_source": pk["source"],
+              "floor_us": round(1e6 * max(t_hbm, t_tc), 2), "frac_of_floor": round(max(t_hbm, t_tc) / t, 4),
+              "t_hbm_us": round(1e6 * t_hbm, 2), "t_tc_sustained_us": round(1e6 * t_tc, 2)}
     if t_tc > t_hbm:
         ach = flops / t / 1e12
-        return {"bound": "tensor", "achieved": round(ach, 1), "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
-                "frac": round(ach / pk["bf16_tflops"], 4), "traffic": traffic,
-                "kernel": kname, "kernel_us": round(t * 1e6, 2),
-                "algorithmic_bytes": byts, "peak_source": pk["source"]}
+        return {"bound": "tensor", "achieved": round(ach, 1), "peak": pk["bf16_tflops_sustained"],
+                "unit": "TFLOP/s", "frac": round(ach / pk["bf16_tflops_sustained"], 4),
+                "peak_kind": "bf16_tflops_sustained", **common}
     ach = byts / t / 1e9
     return {"bound": "hbm", "achieved": round(ach, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
-            "frac": round(ach / pk["hbm_gbs"], 4), "traffic": traffic, "kernel": kname,
-            "kernel_us": round(t * 1e6, 2), "algorithmic_bytes": byts, "peak_source": pk["source"],
-            "frac_of_nominal_8TBps": round(ach / 8000.0, 4)}
+            "frac": round(ach / pk["hbm_gbs"], 4), "peak_kind": "hbm_gbs (copy)",
+            "frac_of_nominal_8TBps": round(ach / 8000.0, 4), **common}
+
+
+def stage1_time_ms(fs, fn, n):
+    """Live CUDA events around each stage-1 launch inside the library (option time_stage1, which
+    also disables PDL for those launches); average launch duration."""
+    fs.set_option("time_stage1", 1)
+    fs.query("stage1_ms")
+    time_loop(fn, n, 2)
+    launches = fs.query("stage1_launches")
+    t = fs.query("stage1_ms") / max(1.0, launches)
+    fs.set_option("time_stage1", 0)
+    return t
 
 
 def run_single(args):
@@ -368,28 +503,24 @@ def run_single(args):
     out = torch.empty(B, dtype=torch.int32, device=dev)
     ctr = [0]
     fn = fused_step_fn(fs, wl, ctr, out)
-    fs.set_option("pdl_w", 1)            # serving configuration: W prefetched across steps (PDL)
     one_kernel = not wl["group_size"]   # plain / transformed sampling: stage 1 finalizes (fuse_reduce)
-    for _ in range(max(3, args.warmup)):
-        fn()
-    torch.cuda.synchronize()
-    with ClockSampler(0) as clk:
-        ms = time_loop(fn, args.steps, args.warmup)
-    clocks = clk.summary()
+    # headline: K back-to-back steps, no cross-step overlap (each kernel waits for the previous one)
+    fs.set_option("pdl_w", 0)
+    ms, clocks = timed_region(fn, args.steps, args.warmup)
     us = ms * 1e3
-    # isolated stage-1 timing (CUDA events around each fused-kernel launch on its stream; PDL off)
-    fs.set_option("time_stage1", 1)
-    fs.query("stage1_ms")
-    time_loop(fn, min(args.steps, 200), 2)
-    launches = fs.query("stage1_launches")
-    t1_ms = fs.query("stage1_ms") / max(1.0, launches)
-    fs.set_option("time_stage1", 0)
+    t1_ms = stage1_time_ms(fs, fn, min(args.steps, 200))
+    per_call = 1e3 * time_median(fn, 100, 25)
+    # PDL-pipelined period: step n+1's W stream starts under step n's tail (reported, not the value)
+    fs.set_option("pdl_w", 1)
+    pipe_ms = time_loop(fn, max(args.steps, 100), args.warmup)
+    fs.set_option("pdl_w", 0)
     # one kernel per step: its average launch duration is the timed loop's events / K
     roof = roofline(name, B, D, V, ms if one_kernel else t1_ms, pk, transforms)
-    roof["timing"] = ("CUDA events over the K timed steps (one fused kernel per step)" if one_kernel
-                      else "CUDA events around each stage-1 launch (PDL off)")
+    roof["timing"] = ("CUDA events over the K timed steps (one fused kernel per step, no PDL overlap)" if one_kernel
+                      else "CUDA events around each stage-1 launch")
     roof["kernel_us_isolated"] = round(t1_ms * 1e3, 2)
-    # end to end through the public API with host buffers (H2D of h [+tau, mask], D2H of idx)
+    # end to end through the public API with host buffers: every step stages this step's h from pinned
+    # host memory, samples, and the host reads the step's ids (stream sync per step, as a serving loop)
     h_host = wl["h"].cpu().pin_memory()
     t_host = wl["temperature"].cpu().pin_memory() if wl["temperature"] is not None else None
     m_host = wl["mask"].cpu().pin_memory() if wl["mask"] is not None else None
@@ -398,24 +529,34 @@ def run_single(args):
     m_dev = torch.empty_like(wl["mask"]) if m_host is not None else None
     idx_host = torch.empty(B, dtype=torch.int32, pin_memory=True)
     e_ctr = [0]
+    stream = torch.cuda.current_stream()
+    sink = [0]
 
     def e2e_fn():
         e_ctr[0] += 1
         fs.sample_from_host(h_host, wl["W"], temperature_host=t_host, mask_host=m_host, bias=wl["bias"],
                             seed=synth.SAMPLING_SEED, step=e_ctr[0], h_dev=h_dev, t_dev=t_dev, m_dev=m_dev,
                             idx_dev=out, idx_host=idx_host)
+        stream.synchronize()
+        sink[0] += int(idx_host[0])
+    # the host syncs every step, so nothing overlaps across steps; pdl_w = 1 only lets this step's
+    # W stream start while the kernel itself is still staging h from host memory
+    fs.set_option("pdl_w", 1)
     e2e_ms = time_loop(e2e_fn, args.steps, args.warmup)
+    fs.set_option("pdl_w", 0)
     h2d = h_host.numel() * 2 + (t_host.numel() * 4 if t_host is not None else 0) + \
         (m_host.numel() * 4 if m_host is not None else 0)
     line = {"metric": METRIC, "value": round(us, 2), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded h~N(0,1), W~N(0,0.02^2), bf16; random-init LM head)",
-            "config": {"workload": f"{name} LM head, B={B}" + (f", grouped g={wl['group_size']}" if n_groups else ""),
-                       "B": B, "D": D, "V": V, "parallelism": "single GPU",
-                       "launch": ("one fused kernel per step" if one_kernel else "stage 1 + stage-2 reduce")
-                                 + ", PDL across steps (pdl_w=1)",
-                       "l2": "no flush: W (%.2f GB) > L2 (126 MB) is re-streamed from HBM every step" % (2 * V * D / 1e9)},
+            "config": config_dict(name, B),
+            "launch": ("one fused kernel per step (stage 2 in the last CTA)" if one_kernel
+                       else "stage 1 + PDL-chained stage-2 reduce") + "; no cross-step overlap (pdl_w=0)",
+            "per_call_median_us": round(per_call, 2),
+            "pipelined_us": round(pipe_ms * 1e3, 2),
+            "pipelined_note": "K back-to-back steps with pdl_w=1: the next step's W stream starts before the "
+                              "previous step's kernel ends (PDL); a period, not a step latency",
             "hbm_gbs_achieved_step": round(algorithmic_bytes(B, D, V, transforms, n_groups) / (ms * 1e-3) / 1e9, 1),
             "roofline": roof,
             "clocks": clocks,
@@ -423,24 +564,24 @@ def run_single(args):
             "e2e": {"value": round(e2e_ms * 1e3, 2), "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": B * 4,
                     "path": ("sample_from_host -> fs_sample_staged: the sampling kernel copies the pinned host h "
-                             "into device memory itself (per-CTA slices + grid counter) and stores the ids into "
-                             "pinned host memory -- one kernel per step" if m_host is None else
+                             "into device memory itself and stores the ids into pinned host memory; the host "
+                             "synchronises and reads the ids every step" if m_host is None else
                              "sample_from_host: pinned inputs staged by fs_copy_async (PDL-chained copy kernel), "
-                             "ids stored by the sampling kernel into pinned host memory")}}
+                             "ids stored by the sampling kernel into pinned host memory; host sync + read every step")}}
     if not args.no_sweep:
         line["sweep"] = sweep(fs, name, pk, args)
-        # the other BASELINE.json configs (same protocol): transforms, grouped, 70B LM head
         if name == "llama3_8b" and not args.no_configs:
-            line["configs"] = {c: sweep(fs, c, pk, args, Bs=(1, 32, 256))
-                               for c in ("qwen25_7b", "gemma3_27b", "llama3_70b")}
+            # the other BASELINE.json configs (same protocol) + the paper's own B200 workload
+            line["configs"] = {c: sweep(fs, c, pk, args) for c in ("qwen25_7b", "gemma3_27b", "llama3_70b")}
+            line["configs"]["paper_d4096"] = sweep(fs, "paper_d4096", pk, args, Bs=PAPER_B)
+            line["tp_shards"] = tp_shards(fs, pk)
+            line["tp_exchange_world1"] = tp_exchange_world1(fs)
     if not args.no_cpu:
-        cus, cores, sample = cpu_oracle_step_us(name, B, args.cpu_seconds)
-        line["cpu_baseline"] = {"value": round(cus, 1), "unit": UNIT, "cores": cores, "kind": "oracle",
-                                "sample": sample}
+        line["cpu_baseline"] = cpu_baseline(name, B, args.cpu_seconds)
     print(json.dumps(line), flush=True)
 
 
-def sweep(fs, name, pk, args, Bs=(1, 8, 32, 128, 256)):
+def sweep(fs, name, pk, args, Bs=SWEEP_B):
     res = {}
     dev = torch.device("cuda", 0)
     for B in Bs:
@@ -450,20 +591,19 @@ def sweep(fs, name, pk, args, Bs=(1, 8, 32, 128, 256)):
         out = torch.empty(B, dtype=torch.int32, device=dev)
         ctr = [0]
         fn = fused_step_fn(fs, wl, ctr, out)
-        fs.set_option("pdl_w", 1)
         one_kernel = not wl["group_size"]
+        fs.set_option("pdl_w", 0)
         us = 1e3 * time_median(fn, 100, 25)            # per-call events (the paper's protocol)
-        loop_us = 1e3 * time_loop(fn, 100, 10)          # back-to-back steps (PDL overlap), as the headline
-        fs.set_option("time_stage1", 1)
-        fs.query("stage1_ms")
-        time_loop(fn, 50, 2)
-        t1 = fs.query("stage1_ms") / 50
-        fs.set_option("time_stage1", 0)
-        r = {"fused_us": round(us, 2), "fused_loop_us": round(loop_us, 2), "stage1_us": round(t1 * 1e3, 2),
-             "one_kernel": one_kernel}
+        loop_us = 1e3 * time_loop(fn, 100, 10)          # back-to-back steps, no overlap (as the headline)
+        t1 = stage1_time_ms(fs, fn, 50)
+        fs.set_option("pdl_w", 1)
+        pipe_us = 1e3 * time_loop(fn, 100, 10)          # PDL-pipelined period
+        fs.set_option("pdl_w", 0)
+        r = {"fused_us": round(us, 2), "fused_loop_us": round(loop_us, 2), "pipelined_us": round(pipe_us, 2),
+             "stage1_us": round(t1 * 1e3, 2), "one_kernel": one_kernel}
         r["roofline"] = roofline(name, B, D, V, us * 1e-3 if one_kernel else t1, pk, transforms)
-        if name == "llama3_8b" and not wl["group_size"]:
-            # SURVEY f3/f4 variants of the same step: per-request RNG streams, log-probabilities
+        if name == "llama3_8b":
+            # SURVEY f1/f3/f4 variants of the same step: per-request RNG streams, log-probabilities, top-k/p
             seeds = torch.arange(B, device=dev, dtype=torch.int64) * 7919 + 17
             vctr = [0]
 
@@ -474,51 +614,157 @@ def sweep(fs, name, pk, args, Bs=(1, 8, 32, 128, 256)):
             def with_logprob():
                 vctr[0] += 1
                 fs.sample(wl["h"], wl["W"], seed=synth.SAMPLING_SEED, step=vctr[0], return_logprob=True)
+
             def topk_fused():
                 vctr[0] += 1
                 fs.sample(wl["h"], wl["W"], seed=synth.SAMPLING_SEED, step=vctr[0], top_k=50, top_p=0.95, out=out)
             r["variants"] = {"per_request_seeds_us": round(1e3 * time_median(per_request, 100, 25), 2),
                              "with_logZ_logprob_us": round(1e3 * time_median(with_logprob, 100, 25), 2),
-                             # SURVEY f1 through the LM head (vs baselines.fi1_gemm_top_k_top_p_us)
                              "top_k50_top_p095_fused_us": round(1e3 * time_median(topk_fused, 100, 25), 2)}
-        if not args.no_baselines and not wl["group_size"]:
-            # standalone sampling over the same materialised fp32 logits (§5.2):
-            # fs_sample_logits vs FlashInfer's Gumbel-max sampling_from_logits (FI2's sampler)
+        if not args.no_baselines and name == "llama3_8b":
+            # standalone sampling over the same materialised fp32 logits (§5.2)
             lg = torch.matmul(wl["h"], wl["W"].t()).float()
             sctr = [0]
 
             def ours_sl():
                 sctr[0] += 1
-                fs.sample_logits(lg, bias=wl["bias"], temperature=wl["temperature"], mask=wl["mask"],
-                                 seed=synth.SAMPLING_SEED, step=sctr[0])
+                fs.sample_logits(lg, seed=synth.SAMPLING_SEED, step=sctr[0])
+
             def ours_topk():
                 sctr[0] += 1
-                fs.sample_logits(lg, bias=wl["bias"], temperature=wl["temperature"], mask=wl["mask"],
-                                 seed=synth.SAMPLING_SEED, step=sctr[0], top_k=50, top_p=0.95)
+                fs.sample_logits(lg, seed=synth.SAMPLING_SEED, step=sctr[0], top_k=50, top_p=0.95)
             st = {"fs_sample_logits_us": round(1e3 * time_median(ours_sl, 100, 25), 2),
                   "fs_sample_logits_top_k50_top_p095_us": round(1e3 * time_median(ours_topk, 100, 25), 2),
                   "logits_bytes": lg.numel() * 4}
             st["fs_sample_logits_gbs"] = round(st["logits_bytes"] / (st["fs_sample_logits_us"] * 1e-6) / 1e9, 1)
             try:
                 import flashinfer.sampling as fis
-                if wl["bias"] is None:
-                    st["flashinfer_sampling_from_logits_us"] = round(
-                        1e3 * time_median(lambda: fis.sampling_from_logits(lg), 100, 25), 2)
-                    st["flashinfer_top_k_top_p_k50_p095_us"] = round(
-                        1e3 * time_median(lambda: fis.top_k_top_p_sampling_from_logits(lg, 50, 0.95), 100, 25), 2)
+                st["flashinfer_sampling_from_logits_us"] = round(
+                    1e3 * time_median(lambda: fis.sampling_from_logits(lg), 100, 25), 2)
+                st["flashinfer_top_k_top_p_k50_p095_us"] = round(
+                    1e3 * time_median(lambda: fis.top_k_top_p_sampling_from_logits(lg, 50, 0.95), 100, 25), 2)
             except Exception as e:  # pragma: no cover
                 st["flashinfer_error"] = repr(e)[:200]
             r["standalone_logits"] = st
             del lg
         if not args.no_baselines:
-            bl = baselines(wl, 100, 25)
+            bl = baselines(name, wl, 100, 25, compiled=not args.no_compile)
             r["baselines"] = {k: (round(v, 2) if isinstance(v, float) else v) for k, v in bl.items()}
             unfused = [v for k, v in bl.items() if k.endswith("_us") and k != "cublas_gemm_only_us"]
             if unfused:
                 r["speedup_vs_best_unfused"] = round(min(unfused) / us, 3)
+            r["speedup_vs_cublas_gemm_only"] = round(bl["cublas_gemm_only_us"] / us, 3)
+            if name == "paper_d4096":
+                mult = bl.get("multinomial_compiled_us", bl["multinomial_eager_us"])
+                ours = {"vs_multinomial": round(mult / us, 3)}
+                if "fi1_gemm_top_k_top_p_us" in bl:
+                    ours["vs_fi1"] = round(bl["fi1_gemm_top_k_top_p_us"] / us, 3)
+                    ours["vs_fi2"] = round(bl["fi2_gemm_sampling_from_logits_us"] / us, 3)
+                r["paper_table3"] = {"ours": ours, "paper_triton_b200": dict(zip(
+                    ("vs_multinomial", "vs_fi1", "vs_fi2"), PAPER_TABLE3_B200.get(B, (None,) * 3)))}
         res[f"B{B}"] = r
         del wl
         torch.cuda.empty_cache()
+    return res
+
+
+def tp_shards(fs, pk, name="llama3_70b", worlds=(2, 4, 8), Bs=(1, 32, 256)):
+    """Compute half of the vocabulary-sharded step (Alg. A.4) at n = 2/4/8, measured on this one GPU:
+    rank 0's shard kernel (fs_sample_shard over V/n rows) and the outer selection over n records
+    (fs_combine_summaries).  The exchange itself needs n GPUs (bench --gpus N).  Beside it, the naive
+    TP baseline's compute half (per-rank cuBLAS GEMM [B, V/n]) and the bytes its logits all-gather
+    would receive per rank."""
+    dev = torch.device("cuda", 0)
+    cfg = synth.CONFIGS[name]
+    D, V = cfg["D"], cfg["V"]
+    res = {}
+    fs.set_option("pdl_w", 0)
+    for n in worlds:
+        lo, hi = 0, V // n
+        for B in Bs:
+            wl = make_device_workload(name, B, dev, seed=7 + n + B, V=V, vocab_rows=(lo, hi))
+            summ = fs.Summaries.empty(B, device=dev)
+            gathered = fs.Summaries.empty(n, B, device=dev)
+            ctr = [0]
+
+            def shard():
+                ctr[0] += 1
+                fs.sample_shard(wl["h"], wl["W"], lo, V, seed=synth.SAMPLING_SEED, step=ctr[0], out=summ)
+
+            shard()
+            gathered.raw.copy_(summ.raw.unsqueeze(0).expand(n, B, 3))
+            shard_us = 1e3 * time_median(shard, 100, 25)
+            comb_us = 1e3 * time_median(lambda: fs.combine_summaries(gathered), 100, 25)
+            gemm_us = 1e3 * time_median(lambda: torch.matmul(wl["h"], wl["W"].t()), 100, 25)
+            res[f"n{n}/B{B}"] = {
+                "V_local": hi - lo, "shard_us": round(shard_us, 2), "combine_us": round(comb_us, 2),
+                "roofline": roofline(name, B, D, hi - lo, shard_us * 1e-3, pk, False,
+                                     kname="shard stage 1 (+ stage 2 in-kernel or PDL reduce)",
+                                     traffic_key=(f"{name}_n{n}", B)),
+                "exchange_bytes_per_rank": 12 * B * n,
+                "naive_tp_gemm_us": round(gemm_us, 2),
+                "naive_tp_allgather_bytes_per_rank": 2 * B * (hi - lo) * (n - 1)}
+            del wl
+    torch.cuda.empty_cache()
+    return res
+
+
+def tp_exchange_world1(fs, name="llama3_70b", n=8, Bs=(1, 32, 256)):
+    """Exchange overhead of the two TP paths without a second GPU: a one-rank NCCL communicator
+    (fs_comm_init world 1 -> fs_sample_tp: shard kernel + ncclAllGather of B x 12 B + combine) and a
+    one-rank peer window (fs_sample_tp_push: shard kernel with the fused push + the PDL-chained
+    wait/combine kernel), each against fs_sample_shard alone on the same n=8 shard.  Per-call medians.
+    The transfer over NVLink itself is not in these numbers (a single GPU box)."""
+    dev = torch.device("cuda", 0)
+    cfg = synth.CONFIGS[name]
+    D, V = cfg["D"], cfg["V"]
+    lo, hi = 0, V // n
+    res = {}
+    fs.set_option("pdl_w", 0)
+    try:
+        fs.comm_init(fs.comm_unique_id(), 1, 0)
+        nccl_ok = True
+    except Exception as e:  # pragma: no cover - NCCL not loadable
+        nccl_ok = False
+        res["nccl_error"] = repr(e)[:200]
+    try:
+        fs.comm_window_open([fs.comm_window_create(1, 0, max(Bs))])
+        push_ok = True
+    except Exception as e:  # pragma: no cover
+        push_ok = False
+        res["push_error"] = repr(e)[:200]
+    for B in Bs:
+        wl = make_device_workload(name, B, dev, seed=11 + B, V=V, vocab_rows=(lo, hi))
+        summ = fs.Summaries.empty(B, device=dev)
+        out = torch.empty(B, dtype=torch.int32, device=dev)
+        ctr = [0]
+
+        def shard():
+            ctr[0] += 1
+            fs.sample_shard(wl["h"], wl["W"], lo, V, seed=synth.SAMPLING_SEED, step=ctr[0], out=summ)
+
+        def nccl():
+            ctr[0] += 1
+            fs.sample_tp(wl["h"], wl["W"], lo, V, seed=synth.SAMPLING_SEED, step=ctr[0], out=out)
+
+        def push():
+            ctr[0] += 1
+            fs.sample_tp_push(wl["h"], wl["W"], lo, V, seed=synth.SAMPLING_SEED, step=ctr[0])
+        r = {"shard_only_us": round(1e3 * time_median(shard, 100, 25), 2)}
+        if nccl_ok:
+            r["nccl_world1_us"] = round(1e3 * time_median(nccl, 100, 25), 2)
+            r["nccl_overhead_us"] = round(r["nccl_world1_us"] - r["shard_only_us"], 2)
+        if push_ok:
+            r["push_world1_us"] = round(1e3 * time_median(push, 100, 25), 2)
+            r["push_overhead_us"] = round(r["push_world1_us"] - r["shard_only_us"], 2)
+            r["push_timeouts"] = fs.query("comm_timeouts")
+        res[f"n{n}shard/B{B}"] = r
+        del wl
+    if nccl_ok:
+        fs.comm_destroy()
+    if push_ok:
+        fs.comm_window_destroy()
+    torch.cuda.empty_cache()
     return res
 
 
@@ -544,34 +790,27 @@ def run_tp(args):
     h = torch.randn(B, D, device=dev, generator=g).to(torch.bfloat16)
     g.manual_seed(5678 + rank)
     W = (torch.randn(b - a, D, device=dev, generator=g) * synth.W_STD).to(torch.bfloat16)
+    transport = "nccl" if backend == "nccl" else "torch"
+    if transport == "nccl":
+        tp.NcclComm()                                     # the library's own communicator (fs_comm_init)
     local_s = fs.Summaries.empty(B, device=dev)
     gathered = torch.empty(world, B, 3, dtype=torch.int32, device=dev)
+    idx_buf = torch.empty(B, dtype=torch.int32, device=dev)
     ctr = [0]
-    fs.set_option("pdl_w", 1)            # W of the next shard step streams before the dependency wait
+    fs.set_option("pdl_w", 0)
 
     def step():
         ctr[0] += 1
-        return tp.sample_tp(h, W, a, V, seed=synth.SAMPLING_SEED, step=ctr[0], workspace=(local_s, gathered))
-    for _ in range(max(3, args.warmup)):
-        step()
-    torch.cuda.synchronize()
-    dist.barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        e0.record()
-        for _ in range(args.steps):
-            idx = step()
-        e1.record()
-        torch.cuda.synchronize()
-    dist.barrier()
-    torch.cuda.synchronize()
-    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+        return tp.sample_tp(h, W, a, V, seed=synth.SAMPLING_SEED, step=ctr[0], workspace=(local_s, gathered),
+                            transport=transport, out=idx_buf)
+    ms_l, clocks = timed_region(step, args.steps, args.warmup, device_index=local, barrier=dist.barrier)
+    ms = torch.tensor([ms_l], device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    idx = step()
     allidx = [torch.empty_like(idx) for _ in range(world)]
     dist.all_gather(allidx, idx)
     identical = all(torch.equal(allidx[0], x) for x in allidx)
-    # e2e: per step H2D of h, D2H of idx, through the same public API
+    # e2e: per step H2D of h, the sharded step, D2H of idx and a host read
     h_host = h.cpu().pin_memory()
     h_dev = torch.empty_like(h)
     idx_host = torch.empty(B, dtype=torch.int32, pin_memory=True)
@@ -579,21 +818,39 @@ def run_tp(args):
     def e2e():
         h_dev.copy_(h_host, non_blocking=True)
         ctr[0] += 1
-        i = tp.sample_tp(h_dev, W, a, V, seed=synth.SAMPLING_SEED, step=ctr[0], workspace=(local_s, gathered))
+        i = tp.sample_tp(h_dev, W, a, V, seed=synth.SAMPLING_SEED, step=ctr[0], workspace=(local_s, gathered),
+                         transport=transport, out=idx_buf)
         idx_host.copy_(i, non_blocking=True)
-    for _ in range(args.warmup):
-        e2e()
-    torch.cuda.synchronize()
-    dist.barrier()
-    e0.record()
-    for _ in range(args.steps):
-        e2e()
-    e1.record()
-    torch.cuda.synchronize()
-    e2e_ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+        torch.cuda.current_stream().synchronize()
+        return int(idx_host[0])
+    e2e_l, _ = timed_region(e2e, args.steps, args.warmup, device_index=local, barrier=dist.barrier,
+                            clock_window_s=0.0)
+    e2e_ms = torch.tensor([e2e_l], device=dev)
     dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
-    # the same step with the library's peer-memory exchange instead of the NCCL
-    # all-gather (reported beside the headline; the headline keeps the NCCL path)
+    # naive TP baseline: per-rank logits [B, V/n] bf16 -> all-gather -> sampler on the full row
+    naive = {}
+    try:
+        lg_local = torch.empty(B, b - a, dtype=torch.bfloat16, device=dev)
+        Vl = V // world
+        lg_all = torch.empty(world, B, Vl, dtype=torch.bfloat16, device=dev)
+
+        def naive_step():
+            torch.matmul(h, W[:Vl].t(), out=lg_local[:, :Vl])
+            dist.all_gather_into_tensor(lg_all, lg_local[:, :Vl].contiguous())
+            full = lg_all.permute(1, 0, 2).reshape(B, world * Vl).float()
+            try:
+                import flashinfer.sampling as fis
+                return fis.sampling_from_logits(full)
+            except Exception:
+                return torch.multinomial(torch.softmax(full, -1), 1)
+        n_ms, _ = timed_region(naive_step, args.steps, args.warmup, device_index=local, barrier=dist.barrier,
+                               clock_window_s=0.0)
+        n_t = torch.tensor([n_ms], device=dev)
+        dist.all_reduce(n_t, op=dist.ReduceOp.MAX)
+        naive = {"us_per_step": round(n_t.item() * 1e3, 2), "allgather_bytes_per_rank": 2 * B * Vl * (world - 1)}
+    except Exception as e:  # pragma: no cover
+        naive = {"error": repr(e)[:200]}
+    # the same step with the library's peer-memory exchange instead of NCCL
     push = {}
     ok = torch.ones(1, device=dev)
     try:
@@ -606,18 +863,13 @@ def run_tp(args):
         def pstep():
             ctr[0] += 1
             return fs.sample_tp_push(h, W, a, V, seed=synth.SAMPLING_SEED, step=ctr[0])
-        for _ in range(max(3, args.warmup)):
-            pstep()
-        torch.cuda.synchronize()
-        dist.barrier()
-        e0.record()
-        for _ in range(args.steps):
-            pidx = pstep()
-        e1.record()
-        torch.cuda.synchronize()
-        p_ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+        p_l, _ = timed_region(pstep, args.steps, args.warmup, device_index=local, barrier=dist.barrier,
+                              clock_window_s=0.0)
+        p_ms = torch.tensor([p_l], device=dev)
         dist.all_reduce(p_ms, op=dist.ReduceOp.MAX)
-        ref = tp.sample_tp(h, W, a, V, seed=synth.SAMPLING_SEED, step=ctr[0], workspace=(local_s, gathered))
+        pidx = pstep()
+        ref = tp.sample_tp(h, W, a, V, seed=synth.SAMPLING_SEED, step=ctr[0], workspace=(local_s, gathered),
+                           transport=transport)
         same = torch.tensor([float(torch.equal(ref, pidx))], device=dev)
         dist.all_reduce(same, op=dist.ReduceOp.MIN)
         push = {"us_per_step": round(p_ms.item() * 1e3, 2), "idx_equal_nccl_path": bool(same.item() == 1),
@@ -629,15 +881,16 @@ def run_tp(args):
         line = {"metric": METRIC, "value": round(us, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms.item(), 5), "higher_is_better": False,
                 "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
-                "data": "synthetic (seeded, random-init LM head shards)",
-                "config": {"workload": f"{name} LM head, B={B}, vocab-sharded TP (Alg. A.4)", "B": B, "D": D,
-                           "V": V, "parallelism": f"tp{world} (vocab)",
-                           "l2": "no flush: per-rank shard %.2f GB" % (2 * (b - a) * D / 1e9)},
+                "data": "synthetic (seeded h~N(0,1), W~N(0,0.02^2), bf16; random-init LM head)",
+                "config": config_dict(name, B, world),
+                "launch": f"fs_sample_tp ({transport}): shard kernel + all-gather of B x 12 B + combine; "
+                          "no cross-step overlap (pdl_w=0)",
                 "aggregate_hbm_gbs": round(byts / (ms.item() * 1e-3) / 1e9, 1),
                 "per_rank_hbm_frac": round((2 * (b - a) * D / (ms.item() * 1e-3) / 1e9) / pk["hbm_gbs"], 4),
                 "idx_identical_across_ranks": identical,
+                "naive_tp_logits_allgather": naive,
                 "exchange_push": push,
-                "clocks": clk.summary(), "gpu_launches": 3 * args.steps,
+                "clocks": clocks, "gpu_launches": 3 * args.steps,
                 "e2e": {"value": round(e2e_ms.item() * 1e3, 2), "unit": UNIT, "h2d_bytes_per_step": B * D * 2,
                         "d2h_bytes_per_step": B * 4}}
         print(json.dumps(line), flush=True)
@@ -654,9 +907,10 @@ def main():
     ap.add_argument("--B", type=int, default=32)
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-baselines", action="store_true")
+    ap.add_argument("--no-compile", action="store_true")
     ap.add_argument("--no-configs", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -18,6 +18,10 @@
 
 #define FS_VERSION_STRING "flashsample-b200 0.1.0 (sm_100a)"
 
+// Appended to allocation failures: the first call for a shape on a context allocates its workspace,
+// so under CUDA graph capture that call must have been made once before, on the same stream.
+static const char* const kAllocHint = " (first call of this shape on this context inside CUDA graph capture? call it once outside capture on the same stream)";
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -165,7 +169,7 @@ fs_status group_ranges(fs_ctx* ctx, const fs::SlotLayout& L, int n_groups, const
     lo[k] = (int)(std::lower_bound(grp.begin(), grp.end(), k) - grp.begin());
   int* dev = nullptr;
   cudaError_t e = cudaMalloc(&dev, lo.size() * sizeof(int));
-  if (e != cudaSuccess) return fail(FS_ERR_OOM, "group range cudaMalloc failed");
+  if (e != cudaSuccess) return fail(FS_ERR_OOM, std::string("group range cudaMalloc failed: ") + cudaGetErrorString(e) + kAllocHint);
   e = cudaMemcpy(dev, lo.data(), lo.size() * sizeof(int), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return cuda_fail(e, "group range copy");
   if (ctx->grp_cache.size() >= 16) {
@@ -184,7 +188,7 @@ constexpr int kFinWords = 260;
 fs_status ensure_fin(fs_ctx* ctx) {
   if (ctx->fin_buf) return FS_OK;
   cudaError_t e = cudaMalloc(&ctx->fin_buf, kFinWords * sizeof(unsigned long long));
-  if (e != cudaSuccess) return fail(FS_ERR_OOM, "finalize buffer cudaMalloc failed");
+  if (e != cudaSuccess) return fail(FS_ERR_OOM, std::string("finalize buffer cudaMalloc failed: ") + cudaGetErrorString(e) + kAllocHint);
   e = cudaMemset(ctx->fin_buf, 0, kFinWords * sizeof(unsigned long long));
   if (e != cudaSuccess) return cuda_fail(e, "finalize buffer memset");
   return FS_OK;
@@ -261,7 +265,7 @@ fs_status segment_maps(fs_ctx* ctx, const void* W, int64_t D, int V, int G, int 
   }
   CUtensorMap* dev = nullptr;
   cudaError_t e = cudaMalloc(&dev, maps.size() * sizeof(CUtensorMap));
-  if (e != cudaSuccess) return fail(FS_ERR_OOM, "descriptor cudaMalloc failed");
+  if (e != cudaSuccess) return fail(FS_ERR_OOM, std::string("descriptor cudaMalloc failed: ") + cudaGetErrorString(e) + kAllocHint);
   e = cudaMemcpy(dev, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return cuda_fail(e, "descriptor upload");
   ctx->seg_cache.push_back(fs_ctx::SegEnt{fs_ctx::SegKey{W, D, V, G, unit, gs, ctx->l2promo}, dev, max_seg});
@@ -463,7 +467,7 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
     if (grp_lo) {                             // warp-per-(row, group) stage 2: scratch + row counters
       if (!ctx->grp_rowcnt) {
         e = cudaMalloc(&ctx->grp_rowcnt, 256 * sizeof(int));
-        if (e != cudaSuccess) return fail(FS_ERR_OOM, "group row counter cudaMalloc failed");
+        if (e != cudaSuccess) return fail(FS_ERR_OOM, std::string("group row counter cudaMalloc failed: ") + cudaGetErrorString(e) + kAllocHint);
         e = cudaMemset(ctx->grp_rowcnt, 0, 256 * sizeof(int));
         if (e != cudaSuccess) return cuda_fail(e, "group row counter memset");
       }
@@ -473,7 +477,7 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
         ctx->gscratch = nullptr;
         ctx->gscratch_bytes = 0;
         e = cudaMalloc(&ctx->gscratch, need);
-        if (e != cudaSuccess) return fail(FS_ERR_OOM, "group scratch cudaMalloc failed");
+        if (e != cudaSuccess) return fail(FS_ERR_OOM, std::string("group scratch cudaMalloc failed: ") + cudaGetErrorString(e) + kAllocHint);
         ctx->gscratch_bytes = need;
       }
       gscratch = static_cast<fs::State*>(ctx->gscratch);
@@ -528,7 +532,7 @@ fs_status run_topk_path(fs_ctx* ctx, const PathArgs& a, int k, float top_p, cuda
   const bool spans = !lists && tc && ctx->topk_spans && !a.bias && !a.mask && (a.V + 15) / 16 <= 32768;
   if ((lists || spans) && !ctx->topk_rowcnt) {
     e = cudaMalloc(&ctx->topk_rowcnt, 256 * sizeof(int));
-    if (e != cudaSuccess) return fail(FS_ERR_OOM, "row counter cudaMalloc failed");
+    if (e != cudaSuccess) return fail(FS_ERR_OOM, std::string("row counter cudaMalloc failed: ") + cudaGetErrorString(e) + kAllocHint);
     e = cudaMemset(ctx->topk_rowcnt, 0, 256 * sizeof(int));
     if (e != cudaSuccess) return cuda_fail(e, "row counter memset");
   }
@@ -986,10 +990,10 @@ fs_status fs_comm_window_create(fs_ctx* ctx, int world, int rank, int B_max, fs_
   ctx->comm_off_acks = ctx->comm_off_flags + (((size_t)2 * world * 8 + 127) & ~size_t(127));
   ctx->comm_off_status = ctx->comm_off_acks + (((size_t)world * 8 + 127) & ~size_t(127));
   const size_t bytes = ctx->comm_off_status + 128;   // status: [0] timeouts, [64] push block counter
-  if ((e = cudaMalloc(&ctx->comm_win, bytes)) != cudaSuccess) return fail(FS_ERR_OOM, "window cudaMalloc failed");
+  if ((e = cudaMalloc(&ctx->comm_win, bytes)) != cudaSuccess) return fail(FS_ERR_OOM, std::string("window cudaMalloc failed: ") + cudaGetErrorString(e) + kAllocHint);
   if ((e = cudaMemset(ctx->comm_win, 0, bytes)) != cudaSuccess) return cuda_fail(e, "window memset");
   if ((e = cudaMalloc(&ctx->comm_local, (size_t)B_max * sizeof(fs_summary))) != cudaSuccess)
-    return fail(FS_ERR_OOM, "summary cudaMalloc failed");
+    return fail(FS_ERR_OOM, std::string("summary cudaMalloc failed: ") + cudaGetErrorString(e) + kAllocHint);
   cudaIpcMemHandle_t h;
   if ((e = cudaIpcGetMemHandle(&h, ctx->comm_win)) != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
   static_assert(sizeof(h) <= sizeof(fs_ipc_handle), "IPC handle size");
@@ -1024,7 +1028,7 @@ fs_status fs_comm_window_open(fs_ctx* ctx, const fs_ipc_handle* handles) {
     tab.acks[p] = reinterpret_cast<uint64_t*>(ctx->comm_peer[p] + ctx->comm_off_acks);
   }
   if (!ctx->comm_peertab && (e = cudaMalloc(&ctx->comm_peertab, sizeof(tab))) != cudaSuccess)
-    return fail(FS_ERR_OOM, "peer table cudaMalloc failed");
+    return fail(FS_ERR_OOM, std::string("peer table cudaMalloc failed: ") + cudaGetErrorString(e) + kAllocHint);
   if ((e = cudaMemcpy(ctx->comm_peertab, &tab, sizeof(tab), cudaMemcpyHostToDevice)) != cudaSuccess)
     return cuda_fail(e, "peer table upload");
   ctx->comm_open = true;
@@ -1164,7 +1168,7 @@ fs_status fs_sample_tp(fs_ctx* ctx, fs_dtype dtype, const void* h, const void* W
     ctx->tp_buf = nullptr;
     ctx->tp_bmax = 0;
     if ((e = cudaMalloc(&ctx->tp_buf, (size_t)(1 + world) * B * sizeof(fs_summary))) != cudaSuccess)
-      return fail(FS_ERR_OOM, "TP summary buffer cudaMalloc failed");
+      return fail(FS_ERR_OOM, std::string("TP summary buffer cudaMalloc failed: ") + cudaGetErrorString(e) + kAllocHint);
     ctx->tp_bmax = B;
   }
   fs_summary* local = ctx->tp_buf;

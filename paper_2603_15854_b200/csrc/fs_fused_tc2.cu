@@ -82,16 +82,12 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
     }
     sm100::fence_barrier_init();
   }
-  // Each CTA of the pair passes its own slot word (tmem_slot[rank]) to the collective
-  // cta_group::2 allocation, so the two CTAs' allocator writes never target the same shared-memory
-  // word even where the paired allocator writes through the cluster window (racecheck reported the
-  // shared slot as a write-write hazard between the pair).
-  if (warp == 1) sm100::tmem_alloc_pair(tmem_slot + rank, (uint32_t)p.tmem_cols);
+  if (warp == 1) sm100::tmem_alloc_pair(tmem_slot, (uint32_t)p.tmem_cols);
   sm100::tc_fence_before();
   sm100::cluster_sync();                    // both CTAs' barriers exist before any remote signal
   __syncthreads();                          // CTA-level order for the allocator's smem write (racecheck)
   sm100::tc_fence_after();
-  const uint32_t tmem_base = tmem_slot[rank];
+  const uint32_t tmem_base = *tmem_slot;
   sm100::pdl_launch_dependents();
   if (warp != 0) {
     // every input but W is read past the dependency wait (the producer defers only its h loads)

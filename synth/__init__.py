@@ -14,6 +14,7 @@ Workload shapes (BASELINE.json `configs`):
   qwen25_7b   D=3584, V=152064  bf16  tau=0.7 + bias + 25% mask
   gemma3_27b  D=5376, V=262208  bf16  grouped variant (g=4096, 65 groups)
   llama3_70b  D=8192, V=128256  bf16  vocab-sharded TP
+  paper_d4096 D=4096, V=151936  bf16  the paper's Table 3 workload (context for its ratios)
 """
 from __future__ import annotations
 
@@ -28,6 +29,8 @@ CONFIGS = {
                       temperature=0.7, bias_std=0.5, mask_ban_frac=0.25),
     "gemma3_27b": dict(D=5376, V=262208, dtype="bf16", config_id=3, group_size=4096),
     "llama3_70b": dict(D=8192, V=128256, dtype="bf16", config_id=4),
+    # the paper's own B200 workload (§5.1, Table 3): Qwen3-8B-like LM head
+    "paper_d4096": dict(D=4096, V=151936, dtype="bf16", config_id=5),
 }
 
 # Sampling seed used by every default workload.

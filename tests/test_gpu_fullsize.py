@@ -1,5 +1,5 @@
 """GPU parity at BASELINE.json's full sizes, EVERY row, in the launch configuration bench.py times
-(options pdl_w = 1 and fuse_reduce = 1, i.e. PDL across steps and the one-kernel finalize).
+(fuse_reduce = 1, the one-kernel finalize; pdl_w = 0, the headline, and pdl_w = 1, the pipelined period).
 
 For each configuration the oracle (fp64 over the whole vocabulary, oracle/sampler.py) is run once
 on B = 256 rows, in chunks of 32 rows; the GPU is then run at B in {1, 32, 128, 256} on the first
@@ -88,9 +88,11 @@ def _rows(flat, B):
                               near=flat.near[:B], logZ=flat.logZ[:B])
 
 
-@pytest.fixture(autouse=True)
-def _bench_launch_config():
-    fs.set_option("pdl_w", 1)            # bench.py's configuration (auto: PDL for B <= 128)
+@pytest.fixture(autouse=True, params=[0, 1], ids=["pdl0", "pdl1"])
+def _bench_launch_config(request):
+    # bench.py's two launch configurations: the headline (no cross-step overlap, pdl_w = 0) and the
+    # pipelined period (pdl_w = 1: PDL for batch chunks <= 128), both with the one-kernel finalize
+    fs.set_option("pdl_w", request.param)
     fs.set_option("fuse_reduce", 1)
     yield
     fs.set_option("pdl_w", 0)

@@ -149,12 +149,15 @@ def test_steps_and_seeds_change_samples():
 def test_cuda_graph_capture_replay():
     wl = _gpu(synth.make_workload("llama3_8b", 8, V=3000, D=128))
     idx = torch.empty(8, dtype=torch.int32, device="cuda")
-    fs.sample(wl.h, wl.W, seed=wl.seed, step=5, out=idx)      # grow workspace outside capture
-    ref = idx.clone()
-    idx.zero_()
     g = torch.cuda.CUDAGraph()
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):
+        # contexts are per (device, stream): grow this stream's workspace outside capture
+        fs.sample(wl.h, wl.W, seed=wl.seed, step=5, out=idx)
+        s.synchronize()
+        ref = idx.clone()
+        idx.zero_()
+        s.synchronize()
         with torch.cuda.graph(g, stream=s):
             fs.sample(wl.h, wl.W, seed=wl.seed, step=5, out=idx)
     g.replay()

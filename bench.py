@@ -227,6 +227,33 @@ def time_median(fn, iters, warmup):
     return statistics.median(a.elapsed_time(b) for a, b in evs)
 
 
+def time_graph(fn, n=50, reps=5):
+    """Device time per call of a short, launch-bound call: n calls captured into one CUDA graph on
+    a side stream and replayed (median of `reps` replays) -- per-call event timing of a ~3 us kernel
+    would measure the host's launch overhead instead."""
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fn()
+        s.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(n):
+                fn()
+        g.replay()
+        s.synchronize()
+        ts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            g.replay()
+            b.record(s)
+            s.synchronize()
+            ts.append(a.elapsed_time(b) / n)
+    torch.cuda.current_stream().wait_stream(s)
+    return statistics.median(ts)
+
+
 def timed_region(fn, steps, warmup, device_index=0, clock_window_s=0.12, barrier=None):
     """The contract's timed region: W warm-ups, then a pre-roll of the same step long enough that the
     clock sampler sees >= clock_window_s of this load, then sync (+ barrier), exactly K steps between
@@ -532,17 +559,28 @@ def run_single(args):
     stream = torch.cuda.current_stream()
     sink = [0]
 
-    def e2e_fn():
+    def e2e_generic():
         e_ctr[0] += 1
         fs.sample_from_host(h_host, wl["W"], temperature_host=t_host, mask_host=m_host, bias=wl["bias"],
                             seed=synth.SAMPLING_SEED, step=e_ctr[0], h_dev=h_dev, t_dev=t_dev, m_dev=m_dev,
                             idx_dev=out, idx_host=idx_host)
         stream.synchronize()
         sink[0] += int(idx_host[0])
+    prepared = None
+    if m_host is None and not wl["group_size"]:
+        prepared = fs.HostStepSampler(h_host, wl["W"], bias=wl["bias"], temperature_host=t_host,
+                                      seed=synth.SAMPLING_SEED, h_dev=h_dev, idx_host=idx_host)
+
+    def e2e_prepared():
+        e_ctr[0] += 1
+        prepared(e_ctr[0])
+        prepared.wait()
+        sink[0] += int(idx_host[0])
     # the host syncs every step, so nothing overlaps across steps; pdl_w = 1 only lets this step's
     # W stream start while the kernel itself is still staging h from host memory
     fs.set_option("pdl_w", 1)
-    e2e_ms = time_loop(e2e_fn, args.steps, args.warmup)
+    e2e_ms = time_loop(e2e_prepared if prepared else e2e_generic, args.steps, args.warmup)
+    e2e_generic_ms = time_loop(e2e_generic, args.steps, args.warmup) if prepared else e2e_ms
     fs.set_option("pdl_w", 0)
     h2d = h_host.numel() * 2 + (t_host.numel() * 4 if t_host is not None else 0) + \
         (m_host.numel() * 4 if m_host is not None else 0)
@@ -562,10 +600,11 @@ def run_single(args):
             "clocks": clocks,
             "gpu_launches": (1 if one_kernel else 2) * args.steps * ((B + 255) // 256),
             "e2e": {"value": round(e2e_ms * 1e3, 2), "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": B * 4,
-                    "path": ("sample_from_host -> fs_sample_staged: the sampling kernel copies the pinned host h "
-                             "into device memory itself and stores the ids into pinned host memory; the host "
-                             "synchronises and reads the ids every step" if m_host is None else
+                    "d2h_bytes_per_step": B * 4, "generic_call_us": round(e2e_generic_ms * 1e3, 2),
+                    "path": ("HostStepSampler (prepared fs_sample_staged call): the sampling kernel copies the "
+                             "pinned host h into device memory itself and stores the ids into pinned host memory; "
+                             "the host synchronises and reads the ids every step (generic_call_us: the same through "
+                             "sample_from_host)" if prepared else
                              "sample_from_host: pinned inputs staged by fs_copy_async (PDL-chained copy kernel), "
                              "ids stored by the sampling kernel into pinned host memory; host sync + read every step")}}
     if not args.no_sweep:
@@ -593,14 +632,18 @@ def sweep(fs, name, pk, args, Bs=SWEEP_B):
         fn = fused_step_fn(fs, wl, ctr, out)
         one_kernel = not wl["group_size"]
         fs.set_option("pdl_w", 0)
-        us = 1e3 * time_median(fn, 100, 25)            # per-call events (the paper's protocol)
-        loop_us = 1e3 * time_loop(fn, 100, 10)          # back-to-back steps, no overlap (as the headline)
+        with ClockSampler(0) as clk_call:
+            us = 1e3 * time_median(fn, 100, 25)        # per-call events (the paper's protocol)
+        with ClockSampler(0) as clk_loop:
+            loop_us = 1e3 * time_loop(fn, 100, 10)      # back-to-back steps, no overlap (as the headline)
         t1 = stage1_time_ms(fs, fn, 50)
         fs.set_option("pdl_w", 1)
         pipe_us = 1e3 * time_loop(fn, 100, 10)          # PDL-pipelined period
         fs.set_option("pdl_w", 0)
         r = {"fused_us": round(us, 2), "fused_loop_us": round(loop_us, 2), "pipelined_us": round(pipe_us, 2),
-             "stage1_us": round(t1 * 1e3, 2), "one_kernel": one_kernel}
+             "stage1_us": round(t1 * 1e3, 2), "one_kernel": one_kernel,
+             "clocks": {k: {"sm_mhz": c.get("sm_mhz"), "power_w": c.get("power_w_median"), "reasons": c.get("reasons")}
+                        for k, c in (("call", clk_call.summary()), ("loop", clk_loop.summary()))}}
         r["roofline"] = roofline(name, B, D, V, us * 1e-3 if one_kernel else t1, pk, transforms)
         if name == "llama3_8b":
             # SURVEY f1/f3/f4 variants of the same step: per-request RNG streams, log-probabilities, top-k/p
@@ -694,7 +737,7 @@ def tp_shards(fs, pk, name="llama3_70b", worlds=(2, 4, 8), Bs=(1, 32, 256)):
             shard()
             gathered.raw.copy_(summ.raw.unsqueeze(0).expand(n, B, 3))
             shard_us = 1e3 * time_median(shard, 100, 25)
-            comb_us = 1e3 * time_median(lambda: fs.combine_summaries(gathered), 100, 25)
+            comb_us = 1e3 * time_graph(lambda: fs.combine_summaries(gathered))
             gemm_us = 1e3 * time_median(lambda: torch.matmul(wl["h"], wl["W"].t()), 100, 25)
             res[f"n{n}/B{B}"] = {
                 "V_local": hi - lo, "shard_us": round(shard_us, 2), "combine_us": round(comb_us, 2),

@@ -304,6 +304,9 @@ fs_status fs_comm_window_destroy(fs_ctx* ctx);
  *   -> outer selection (fs_combine_summaries): idx_out [B] identical on every rank, equal to
  *      fs_sample on the unsharded W (global ids; reading R8 max reuse), score_out / logZ_out
  *      optional, per_rank_out [world][B] fs_summary (device) or NULL: the gathered records.
+ *   Without logZ_out and per_rank_out only (M, I) of the records are consumed: the shard then runs
+ *   the plain epilogue and its last CTA writes the records directly (L unused), so no log-mass
+ *   epilogue and no stage-2 kernel run.
  *   Arguments as fs_sample_shard.  Asynchronous; FS_ERR_NCCL when the collective cannot be
  *   enqueued or the communicator reports an asynchronous error (ncclCommGetAsyncError, checked
  *   at every call).

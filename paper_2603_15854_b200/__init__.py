@@ -24,7 +24,8 @@ from ._lib import FS_BF16, FS_F32, FlashSampleError
 __all__ = ["sample", "sample_grouped", "sample_logits", "sample_shard", "combine_summaries", "merge_summaries",
            "random_bits", "gumbel_from_bits", "Summaries", "context", "set_option", "query",
            "FlashSampleError", "version", "sample_from_host", "comm_window_create", "comm_window_open",
-           "comm_window_destroy", "sample_tp_push", "comm_unique_id", "comm_init", "comm_destroy", "sample_tp"]
+           "comm_window_destroy", "sample_tp_push", "comm_unique_id", "comm_init", "comm_destroy", "sample_tp",
+           "HostStepSampler"]
 
 _ctx = {}            # (device, CUDA stream handle) -> fs_ctx handle
 _opts = {}           # device -> {option: value}, applied to every context of that device
@@ -429,3 +430,45 @@ def sample_from_host(h_host, W, *, temperature_host=None, mask_host=None, bias=N
     idx_host = idx_host if idx_host is not None else torch.empty(idx_dev.shape, dtype=torch.int32, pin_memory=True)
     idx_host.copy_(idx_dev, non_blocking=True)
     return idx_host
+
+
+class HostStepSampler:
+    """A serving loop's per-step call, prepared once: the end-to-end step of `sample_from_host`
+    (fs_sample_staged: the sampling kernel stages this step's h from the pinned host buffer itself
+    and stores the ids into the pinned host idx buffer) with every argument validated and marshalled
+    at construction, so a step costs one ctypes call.  The caller rewrites `h_host` (pinned, bf16
+    [B, D]) in place between steps and reads `idx_host` after `wait()`.
+        s = HostStepSampler(h_host, W, seed=...)
+        for t in ...: s(step=t); s.wait(); tok = s.idx_host
+    """
+    def __init__(self, h_host, W, *, bias=None, temperature_host=None, seed: int = 0, h_dev=None, idx_host=None):
+        if h_host.dtype != torch.bfloat16 or h_host.dim() != 2 or not h_host.is_pinned() or not h_host.is_contiguous():
+            raise ValueError("h_host must be a contiguous pinned bf16 [B, D] tensor")
+        if W.dtype != torch.bfloat16 or not W.is_cuda or not W.is_contiguous() or W.shape[1] != h_host.shape[1]:
+            raise ValueError("W must be a contiguous bf16 [V, D] CUDA tensor with D = h_host.shape[1]")
+        B, D = h_host.shape
+        V = W.shape[0]
+        if temperature_host is not None and (temperature_host.dtype != torch.float32 or temperature_host.numel() != B
+                                             or not temperature_host.is_pinned()):
+            raise ValueError("temperature_host must be a pinned fp32 [B] tensor")
+        if bias is not None and (bias.dtype != torch.float32 or bias.numel() != V or not bias.is_cuda):
+            raise ValueError("bias must be a device fp32 [V] tensor")
+        self.h_host, self.W, self.bias, self.temperature_host = h_host, W, bias, temperature_host
+        self.h_dev = h_dev if h_dev is not None else torch.empty_like(h_host, device=W.device)
+        self.idx_host = idx_host if idx_host is not None else torch.empty(B, dtype=torch.int32, pin_memory=True)
+        self.stream = torch.cuda.current_stream(W.device)
+        self._fn = _lib.lib().fs_sample_staged
+        self._head = (context(W.device, self.stream), FS_BF16, _ptr(h_host), _ptr(self.h_dev), _ptr(W), _ptr(bias),
+                      _ptr(temperature_host), None)
+        self._seed = seed & (2**64 - 1)
+        self._tail = (B, D, V, _ptr(self.idx_host), None, ctypes.c_void_p(self.stream.cuda_stream))
+
+    def __call__(self, step: int):
+        st = self._fn(*self._head, self._seed, step & (2**64 - 1), *self._tail)
+        if st:
+            _lib.check(st, "fs_sample_staged")
+        return self.idx_host
+
+    def wait(self):
+        self.stream.synchronize()
+        return self.idx_host

@@ -58,6 +58,9 @@ struct fs_ctx {
   int dbg_no_epi = 0;
   int l2promo = 3;                 // CUtensorMapL2promotion for W/h maps (3 = 256B)
   int w_policy = 1;                // 1: W loads evict_first, 0: no cache hint
+  int spin_wait = 0;               // A/B: epilogue barrier waits without the suspend-time hint
+  int prune = 0;                   // exact Gumbel pruning in the one-kernel epilogue (fs_epilogue.cuh);
+                                   // off: measured no faster (DESIGN.md §11 entry 18)
   int epi_sleep = 0;               // ns of backoff in epilogue barrier waits (0 = spin)
   int unit_rows = 0;               // CTA range granularity (0 = default)
   int pair = -1;                   // CTA-pair kernel: -1 auto (by batch size), 0 off, 1 on
@@ -297,6 +300,7 @@ struct PathArgs {
   const uint64_t* steps = nullptr;
   const void* h_host = nullptr;   // fs_sample_staged: pinned host h, staged into h by the kernel
   const fs::PushCtx* push = nullptr;   // f2: the shard's summaries also go to the peer windows (B <= 256)
+  fs_summary* sum_out = nullptr;       // shard without log-mass: one-kernel finalize writes {M, I, NaN}
 };
 
 // time_stage1 option: record a start event now and return the end event to record after stage 1.
@@ -319,6 +323,13 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
   cudaError_t e = cudaSetDevice(ctx->device);
   if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
   const bool tc = !ctx->force_simt && a.dtype == FS_BF16 && (a.D % 8 == 0) && aligned16(a.h) && aligned16(a.W);
+  if (a.sum_out && !(tc && ctx->fuse_reduce)) {   // no one-kernel finalize here: the log-mass shard path
+    PathArgs b = a;
+    b.lse = true;
+    b.groups_out = a.sum_out;
+    b.sum_out = nullptr;
+    return run_path(ctx, b, stream);
+  }
   const size_t esz = a.dtype == FS_BF16 ? 2 : 4;
   const int unit = ctx->unit_rows > 0 ? ctx->unit_rows : 16;
   const int U = (a.V + unit - 1) / unit;
@@ -340,7 +351,7 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
   const fs::SlotLayout lay{n_slots, tc ? 0 : 1, G, a.V, max_seg, a.group_size, unit, pair ? 1 : 0};
   // one-kernel finalize: the last stage-1 CTA reduces the per-CTA candidates (fs_epilogue.cuh
   // finalize_last_cta) -- single group, no log-mass outputs
-  const bool fin = tc && ctx->fuse_reduce && !a.lse && a.group_size >= a.V && a.idx_out != nullptr;
+  const bool fin = tc && ctx->fuse_reduce && !a.lse && a.group_size >= a.V && (a.idx_out != nullptr || a.sum_out);
   // with log-mass outputs: the last CTA runs the per-row reduce itself (one warp per row; for small
   // B, where a second kernel's launch + grid hop cost more than the serial rows)
   const bool fin_lse = tc && ctx->fuse_reduce && a.lse && a.group_size >= a.V && a.B <= 16;   // measured crossover
@@ -392,6 +403,8 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
       p.dbg_times = ctx->dbg_times;
       p.w_policy = ctx->w_policy;
       p.epi_sleep = ctx->epi_sleep;
+      p.prune = ctx->prune;
+      p.spin_wait = ctx->spin_wait;
       auto stages_for = [&](int k) { return pair ? fs::tc2_stages(BN, k) : fs::tc_stages(BN, k); };
       p.kbps = ctx->kbps;
       if (p.kbps <= 0) {
@@ -411,7 +424,8 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
       if (fin) {
         p.fin_best = ctx->fin_buf;
         p.fin_ctr = reinterpret_cast<unsigned int*>(ctx->fin_buf + 256);
-        p.idx_out = a.idx_out + r0;
+        p.idx_out = a.idx_out ? a.idx_out + r0 : nullptr;
+        p.fin_sum = a.sum_out ? a.sum_out + r0 : nullptr;
         p.score_out = a.score_out ? a.score_out + r0 : nullptr;
         if (a.h_host) {
           const void* hsrc = static_cast<const char*>(a.h_host) + (size_t)r0 * a.D * esz;
@@ -740,6 +754,8 @@ fs_status fs_ctx_set_option(fs_ctx* ctx, const char* name, int64_t value) {
   else if (!strcmp(name, "topk_spans")) ctx->topk_spans = (int)value;
   else if (!strcmp(name, "grp_ranges")) ctx->grp_ranges = (int)value;
   else if (!strcmp(name, "pdl_w")) ctx->pdl_w = (int)value;
+  else if (!strcmp(name, "prune")) ctx->prune = (int)value;
+  else if (!strcmp(name, "spin_wait")) ctx->spin_wait = (int)value;
   else if (!strcmp(name, "pdl_w_max_b")) ctx->pdl_w_max_b = (int)value;
   else if (!strcmp(name, "staging_check")) ctx->staging_check = (int)value;
   else if (!strcmp(name, "dbg_times")) ctx->dbg_times = reinterpret_cast<unsigned long long*>(value);
@@ -865,9 +881,13 @@ fs_status fs_sample_grouped(fs_ctx* ctx, fs_dtype dtype, const void* h, const vo
   return run_path(ctx, a, static_cast<cudaStream_t>(stream));
 }
 
-fs_status fs_sample_shard(fs_ctx* ctx, fs_dtype dtype, const void* h, const void* W_shard, const float* bias_shard,
-                          const float* temperature, const uint32_t* mask, uint64_t seed, uint64_t step, int B, int D,
-                          int V_local, int64_t vocab_offset, int64_t V_total, fs_summary* summary_out, void* stream) {
+// The rank-local half of Alg. A.4.  need_lse = false (fs_sample_tp without logZ / per-rank outputs):
+// only (M, I) of the records are consumed, so the shard runs the plain epilogue with the one-kernel
+// finalize writing the records directly (L = NaN) -- no log-mass epilogue, no stage-2 kernel.
+static fs_status shard_impl(fs_ctx* ctx, fs_dtype dtype, const void* h, const void* W_shard, const float* bias_shard,
+                            const float* temperature, const uint32_t* mask, uint64_t seed, uint64_t step, int B,
+                            int D, int V_local, int64_t vocab_offset, int64_t V_total, fs_summary* summary_out,
+                            bool need_lse, void* stream) {
   fs_status s = check_common(ctx, dtype, h, W_shard, B, D, V_local);
   if (s != FS_OK) return s;
   FS_LOCK(ctx);
@@ -876,7 +896,19 @@ fs_status fs_sample_shard(fs_ctx* ctx, fs_dtype dtype, const void* h, const void
     return fail(FS_ERR_INVALID, "need 0 <= vocab_offset, vocab_offset + V_local <= V_total < 2^31");
   PathArgs a{dtype, h, W_shard, bias_shard, temperature, mask, (V_total + 31) / 32, seed, step, B, D, V_local,
              vocab_offset, ((V_local + 127) / 128) * 128, true, nullptr, nullptr, nullptr, summary_out, 1, nullptr};
+  if (!need_lse) {
+    a.lse = false;
+    a.groups_out = nullptr;
+    a.sum_out = summary_out;
+  }
   return run_path(ctx, a, static_cast<cudaStream_t>(stream));
+}
+
+fs_status fs_sample_shard(fs_ctx* ctx, fs_dtype dtype, const void* h, const void* W_shard, const float* bias_shard,
+                          const float* temperature, const uint32_t* mask, uint64_t seed, uint64_t step, int B, int D,
+                          int V_local, int64_t vocab_offset, int64_t V_total, fs_summary* summary_out, void* stream) {
+  return shard_impl(ctx, dtype, h, W_shard, bias_shard, temperature, mask, seed, step, B, D, V_local, vocab_offset,
+                    V_total, summary_out, true, stream);
 }
 
 static fs_status sample_logits_impl(fs_ctx* ctx, fs_dtype dtype, const void* logits, int64_t ld, const float* bias,
@@ -1173,8 +1205,9 @@ fs_status fs_sample_tp(fs_ctx* ctx, fs_dtype dtype, const void* h, const void* W
   }
   fs_summary* local = ctx->tp_buf;
   fs_summary* gathered = ctx->tp_buf + ctx->tp_bmax;
-  fs_status s = fs_sample_shard(ctx, dtype, h, W_shard, bias_shard, temperature, mask, seed, step, B, D, V_local,
-                                vocab_offset, V_total, local, stream);
+  // without logZ / per-rank outputs only (M, I) matter: the shard skips the log-mass epilogue
+  fs_status s = shard_impl(ctx, dtype, h, W_shard, bias_shard, temperature, mask, seed, step, B, D, V_local,
+                           vocab_offset, V_total, local, logZ_out != nullptr || per_rank_out != nullptr, stream);
   if (s != FS_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // Alg. A.4 line 4: every rank contributes its B x 12-byte message; [world][B] arrives

@@ -66,7 +66,28 @@ struct EpiArgs {
   int row_offset;           // global batch index of column 0 (RNG counter)
   uint32_t k0, k1, c2, c3;  // Philox key and counter words 2, 3
   int dbg_skip;             // debug: drain TMEM without computing (bounds the MMA+TMA-only time)
+  unsigned long long* gbest;  // one-kernel finalize words fin_best[B] ((key << 32) | ~idx, all CTAs):
+                              // non-null = exact Gumbel pruning against the best score so far (below)
 };
+
+// One-kernel finalize (StageOneParams::fin_best).  The candidate order of state_merge (larger key,
+// then smaller id) is the unsigned order of (key << 32 | ~idx), so a 64-bit atomicMax per row
+// reduces the per-CTA candidates in L2 in any arrival order with the same result as stage 2.
+__device__ __forceinline__ unsigned long long pack_state(const State& s) {
+  return ((unsigned long long)s.key << 32) | (unsigned long long)(s.idx >= 0 ? ~(uint32_t)s.idx : 0u);
+}
+
+// Exact pruning of the Gumbel evaluation (plain sampling with the one-kernel finalize).
+// g(r) = -ln(-ln u) < -ln(1 - u) <= (k + 1) ln 2 + 2^-32, k = number of leading one bits of r
+// (u = (r+1)/(2^32+1); -ln u >= 1 - u and 1 - u > 2^-(k+1)).  An element whose upper bound
+// l~ + (k+1) ln 2 (+ margin for the fp32 roundings of l~ + G32) does not exceed the score of a
+// candidate already recorded for its batch row -- this warp's running best or any CTA's published
+// best in fin_best -- has a strictly smaller perturbed score than that candidate, so it is neither
+// the row's argmax nor tied with it: its Gumbel is never evaluated.  The argmax, its id and its
+// score are bit-identical to the unpruned epilogue (tests/test_gpu_prune.py).
+__device__ __forceinline__ float gumbel_upper(uint32_t r, float l) {
+  return (float)(__clz(~r) + 1) * kLn2 + 1e-3f + fabsf(l) * 1e-6f;
+}
 
 struct RowArgs {
   bool valid;               // this lane's vocabulary row is inside the tile
@@ -210,9 +231,16 @@ __device__ __forceinline__ void epi_tile_tc(uint32_t taddr, const RowArgs& ra, c
     release_tmem(tempty, tempty_cluster, lane);
     return;
   }
+  const bool prune = !LSE && ea.gbest != nullptr;
 #pragma unroll 1
   for (int c = chunk0; c < nch; c += cstep) {
     State own = st[0];
+    // pruning threshold of column c*32 + lane: this warp's running best or the best published by
+    // any CTA so far (a stale read is still a recorded candidate's score: a valid threshold)
+    uint32_t thr_lane = own.key;
+    if (prune && c * 32 + lane < B)
+      thr_lane = max(thr_lane, (uint32_t)(__ldcg(ea.gbest + c * 32 + lane) >> 32));
+    const uint32_t thr_in = thr_lane;
 #pragma unroll 1
     for (int g = 0; g < 4; g += NG) {
       const int col0 = c * 32 + g * 8;
@@ -239,10 +267,10 @@ __device__ __forceinline__ void epi_tile_tc(uint32_t taddr, const RowArgs& ra, c
         if ((lane & 15) < NC && jb < B && w < ea.mask_words) mw = __ldg(ea.mask + (int64_t)jb * ea.mask_words + w);
       }
       // randomness: independent of the accumulator, overlaps the TMEM load
-      float gm[NC];
+      uint32_t rb[NC];
       if (PRQ && (ra.warp_v0 & 3)) {             // unaligned shard offset: one Philox per element
 #pragma unroll
-        for (int jj = 0; jj < NC; ++jj) gm[jj] = gumbel32(per_request_bits(ea.tab, ra.v_lo, col0 + jj));
+        for (int jj = 0; jj < NC; ++jj) rb[jj] = per_request_bits(ea.tab, ra.v_lo, col0 + jj);
       } else if (PRQ) {                          // lane quartets share v >> 2: one Philox per 4 elements
 #pragma unroll
         for (int qq = 0; qq < NC / 4; ++qq) {
@@ -250,19 +278,67 @@ __device__ __forceinline__ void epi_tile_tc(uint32_t taddr, const RowArgs& ra, c
           uint32_t rr[4];
           prq_bits4(ra.v_lo >> 2, ea.tab->k0[bq], ea.tab->k1[bq], ea.tab->c2[bq], ea.tab->c3[bq], lane, rr);
 #pragma unroll
-          for (int c = 0; c < 4; ++c) gm[4 * qq + c] = gumbel32(rr[c]);
+          for (int c = 0; c < 4; ++c) rb[4 * qq + c] = rr[c];
         }
       } else {
         const uint32_t qd = (uint32_t)(ea.row_offset + col0) >> 2;
 #pragma unroll
         for (int qq = 0; qq < NC / 4; ++qq) {
           const U4 p4 = philox4x32_10(ra.v_lo, qd + (uint32_t)qq, ea.c2, ea.c3, ea.k0, ea.k1);
-          gm[4 * qq + 0] = gumbel32(p4.x);
-          gm[4 * qq + 1] = gumbel32(p4.y);
-          gm[4 * qq + 2] = gumbel32(p4.z);
-          gm[4 * qq + 3] = gumbel32(p4.w);
+          rb[4 * qq + 0] = p4.x;
+          rb[4 * qq + 1] = p4.y;
+          rb[4 * qq + 2] = p4.z;
+          rb[4 * qq + 3] = p4.w;
         }
       }
+      if (prune) {
+        sm100::tmem_wait_ld();
+        if (col0 + NC >= B || (c + cstep >= nch && g + NG >= 4))      // this warp's last TMEM read
+          release_tmem(tempty, tempty_cluster, lane);
+        // l~ and the bound test per element; only columns with a surviving element evaluate G32
+        float lt[NC];
+        uint32_t pm = 0u;
+#pragma unroll
+        for (int jj = 0; jj < NC; ++jj) {
+          float l = __uint_as_float(r[jj]);
+          float gs = 1.0f;
+          if (XFORM) {
+            l = (l + ra.bias) * ea.invtau[col0 + jj];
+            gs = ea.tab->gscale[col0 + jj];
+            if (ea.mask != nullptr) {
+              const uint32_t w = __shfl_sync(0xFFFFFFFFu, mw, msrc + jj);
+              if (!((w >> mbit) & 1u)) l = -INFINITY;
+            }
+          }
+          if (isnan(l)) l = -INFINITY;
+          lt[jj] = l;
+          const uint32_t thr = __shfl_sync(0xFFFFFFFFu, thr_lane, g * 8 + jj);
+          const bool pass = ra.valid && (thr == kKeyNone || l + gumbel_upper(rb[jj], l) * gs > key_ref(thr));
+          pm |= (uint32_t)pass << jj;
+        }
+        const uint32_t cols = __reduce_or_sync(0xFFFFFFFFu, pm);
+        const int jo = lane - g * 8;
+        uint32_t km = 0u, bl = 0u;
+#pragma unroll
+        for (int jj = 0; jj < NC; ++jj) {
+          if (cols & (1u << jj)) {                                       // warp-uniform
+            const float gj = XFORM ? gumbel32(rb[jj]) * ea.tab->gscale[col0 + jj] : gumbel32(rb[jj]);
+            const uint32_t key = ((pm >> jj) & 1u) ? order_key(lt[jj] + gj) : kKeyNone;
+            const uint32_t kx = __reduce_max_sync(0xFFFFFFFFu, key);
+            const uint32_t bx = __ballot_sync(0xFFFFFFFFu, key == kx);
+            km = (jo == jj) ? kx : km;
+            bl = (jo == jj) ? bx : bl;
+          }
+        }
+        const int32_t wi = km > kKeyNone ? ra.warp_v0 + (__ffs(bl) - 1) : -1;
+        const bool upd = (unsigned)jo < (unsigned)NC && (km > own.key);  // ties keep the earlier id
+        own.key = upd ? km : own.key;
+        own.idx = upd ? wi : own.idx;
+        continue;
+      }
+      float gm[NC];
+#pragma unroll
+      for (int jj = 0; jj < NC; ++jj) gm[jj] = gumbel32(rb[jj]);
       sm100::tmem_wait_ld();
       if (col0 + NC >= B || (c + cstep >= nch && g + NG >= 4))        // this warp's last TMEM read
         release_tmem(tempty, tempty_cluster, lane);
@@ -347,6 +423,9 @@ __device__ __forceinline__ void epi_tile_tc(uint32_t taddr, const RowArgs& ra, c
         own.idx = upd ? wi : own.idx;
       }
     }
+    // publish an improved best of column c*32 + lane for every CTA's pruning (the final fold is a
+    // max over the same candidates, so early publication does not change the result)
+    if (prune && c * 32 + lane < B && own.key > thr_in) atomicMax(ea.gbest + c * 32 + lane, pack_state(own));
     st[0] = own;
     if (nmine > 1) rotate_states(st);
   }
@@ -368,22 +447,19 @@ __device__ __forceinline__ void flush_warp(State (&st)[NST], int lane, int B, St
   }
 }
 
-// One-kernel finalize (StageOneParams::fin_best).  The candidate order of state_merge (larger key,
-// then smaller id) is the unsigned order of (key << 32 | ~idx), so a 64-bit atomicMax per row
-// reduces the per-CTA candidates in L2 in any arrival order with the same result as stage 2.
-__device__ __forceinline__ unsigned long long pack_state(const State& s) {
-  return ((unsigned long long)s.key << 32) | (unsigned long long)(s.idx >= 0 ? ~(uint32_t)s.idx : 0u);
-}
+// One-kernel finalize, last step (pack_state above).
 // Called by all `nthr` epilogue threads (ids et) of every CTA after their atomicMax calls: the last
 // CTA to arrive (threadFenceReduction pattern) converts the row maxima to (idx, score) exactly as
 // stage 2's to_summary does, and leaves fin_best / fin_ctr at 0 for the next call.
 // With in-kernel staging (h_bar != nullptr), h_bar[1] is the staging-timeout flag (wait_h_staged):
 // when set, h was not fully staged before some CTA's first h load, so every row is reported
 // undefined (idx -1, score -inf) and h_bar[2] counts the event (fs_ctx_query "staging_timeouts").
+// With sum_out (a TP shard step that needs no log-mass, fs_sample_tp without logZ) the row maxima are
+// written as the shard's exchange records {M, I, L = NaN} instead of idx / score.
 __device__ __forceinline__ void finalize_last_cta(unsigned long long* best, unsigned int* ctr, int B,
                                                   int32_t* idx_out, float* score_out, int et, int nthr,
                                                   uint32_t bar_id, volatile int* flag, unsigned n_ctas,
-                                                  unsigned int* h_bar = nullptr) {
+                                                  unsigned int* h_bar = nullptr, fs_summary* sum_out = nullptr) {
   __threadfence();
   sm100::named_bar_sync(bar_id, nthr);
   if (et == 0) *flag = (atomicAdd(ctr, 1u) == n_ctas - 1) ? 1 : 0;
@@ -395,8 +471,11 @@ __device__ __forceinline__ void finalize_last_cta(unsigned long long* best, unsi
       const unsigned long long v = atomicExch(&best[b], 0ull);
       const uint32_t key = (uint32_t)(v >> 32);
       const bool defined = key > kKeyNegInf && !timed_out;
-      idx_out[b] = defined ? (int32_t)~(uint32_t)v : -1;
-      if (score_out) score_out[b] = defined ? key_to_float(key) : -INFINITY;
+      const int32_t id = defined ? (int32_t)~(uint32_t)v : -1;
+      const float sc = defined ? key_to_float(key) : -INFINITY;
+      if (idx_out) idx_out[b] = id;
+      if (score_out) score_out[b] = sc;
+      if (sum_out) sum_out[b] = fs_summary{sc, id, __int_as_float(0x7FC00000)};
     }
     sm100::named_bar_sync(bar_id, nthr);     // every thread read the timeout flag
     if (et == 0) {

@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(128) fused_simt_kernel(const StageOneParams p)
   ra.v_lo = (uint32_t)ra.v_global;
   ra.warp_v0 = (int32_t)(p.vocab_offset + base + 32 * q);
   ra.bias = (ra.valid && p.bias) ? p.bias[row] : 0.0f;
-  EpiArgs ea;
+  EpiArgs ea{};
   ea.invtau = tab.invtau;
   ea.tab = &tab;
   ea.mask = p.mask;

@@ -292,6 +292,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
     ea.c2 = ctr_step_lo(p.step);
     ea.c3 = ctr_step_hi(p.step, 0u);
     ea.dbg_skip = p.dbg_no_epi;
+    ea.gbest = (!LSE && p.prune) ? p.fin_best : nullptr;   // exact Gumbel pruning (fs_epilogue.cuh)
     State st[8];
 #pragma unroll
     for (int c = 0; c < 8; ++c) st[c] = state_empty();
@@ -304,6 +305,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
         const int t1 = min(b, t0 + kBlockM);
         const uint32_t use = (uint32_t)(tile_i >> 1);
         if (p.epi_sleep) sm100::mbar_wait_sleep(&tfull[set], use & 1, (uint32_t)p.epi_sleep);
+        else if (p.spin_wait) sm100::mbar_wait_spin(&tfull[set], use & 1);   // A/B only
         else sm100::mbar_wait(&tfull[set], use & 1);
         sm100::tc_fence_after();
         const int row = t0 + 32 * q + lane;     // TMEM lane l of this tile = row t0 + l
@@ -359,7 +361,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
       }
       if (p.fin_best)
         finalize_last_cta(p.fin_best, p.fin_ctr, p.B, p.idx_out, p.score_out, et, 32 * kEpiWarps, 1,
-                          reinterpret_cast<volatile int*>(scratch + kEpiWarps * BN), gridDim.x, p.h_bar);
+                          reinterpret_cast<volatile int*>(scratch + kEpiWarps * BN), gridDim.x, p.h_bar, p.fin_sum);
       else if (et == 0)
         p.part_group[blockIdx.x] = (r0 < r1) ? 0 : -1;
       if (!p.fin_best && p.fin_lse)

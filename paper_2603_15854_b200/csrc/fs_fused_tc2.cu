@@ -42,7 +42,7 @@ __device__ __forceinline__ int seg_end2(int a, int r1, int gs) { return min(r1, 
 }  // namespace
 
 template <bool LSE, bool XFORM, bool PRQ>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 1)   // 18 warps: <= 96 registers (5 warps on a 16K-register SM sub-partition)
 fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p) {
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned base by pointer arithmetic on the shared array, so that every pointer derived
@@ -216,6 +216,7 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
     ea.c2 = ctr_step_lo(p.step);
     ea.c3 = ctr_step_hi(p.step, 0u);
     ea.dbg_skip = p.dbg_no_epi;
+    ea.gbest = (!LSE && p.prune) ? p.fin_best : nullptr;   // exact Gumbel pruning (fs_epilogue.cuh)
     const uint32_t tempty_leader = sm100::mapa(sm100::smem_u32(&tempty[set]), 0);
     State st[4];
 #pragma unroll
@@ -227,7 +228,8 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
       for (int t0 = a; t0 < b; t0 += 256, ++tile_i) {
         if ((tile_i & 1) != set) continue;
         const uint32_t use = (uint32_t)(tile_i >> 1);
-        sm100::mbar_wait(&tfull[set], use & 1);
+        if (p.spin_wait) sm100::mbar_wait_spin(&tfull[set], use & 1);   // A/B only
+        else sm100::mbar_wait(&tfull[set], use & 1);
         sm100::tc_fence_after();
         const int base = t0 + 128 * (int)rank;
         const int row = base + 32 * q + lane;
@@ -280,7 +282,7 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
       }
       if (p.fin_best)
         finalize_last_cta(p.fin_best, p.fin_ctr, p.B, p.idx_out, p.score_out, et, 32 * kEpiWarps, 1,
-                          reinterpret_cast<volatile int*>(scratch + kSlotWarps * BN), gridDim.x, p.h_bar);
+                          reinterpret_cast<volatile int*>(scratch + kSlotWarps * BN), gridDim.x, p.h_bar, p.fin_sum);
       else if (et == 0)
         p.part_group[blockIdx.x] = (r0 < r1) ? 0 : -1;
       if (!p.fin_best && p.fin_lse)

@@ -76,6 +76,9 @@ struct StageOneParams {
   // into fin_best[b] by a 64-bit atomicMax of (key << 32 | ~idx); the last CTA to finish (fin_ctr)
   // writes idx_out / score_out and resets both, so no stage-2 launch follows.
   unsigned long long* fin_best;   // [256], all 0 between calls; nullptr = write `part` for stage 2
+  int spin_wait;                  // A/B: epilogue waits spin on try_wait without the suspend hint
+  fs_summary* fin_sum;            // with fin_best: write {M, I, L = NaN} records instead of idx / score
+  int prune;                      // with fin_best: skip G32 where a recorded best provably wins
   unsigned int* fin_ctr;          // CTAs finished, 0 between calls
   int32_t* idx_out;               // [B] of this chunk
   float* score_out;               // [B] or nullptr

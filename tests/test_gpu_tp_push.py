@@ -113,3 +113,25 @@ def test_nccl_sample_tp_world1_equals_single_gpu():
     _, flat = oracle_flat(wl, 2)
     check_flat(idx.cpu().numpy(), score.cpu().numpy(), flat)
     fs.comm_destroy()
+
+
+def test_nccl_sample_tp_idx_only_skips_log_mass_and_matches():
+    """fs_sample_tp without logZ / per-rank outputs runs the shard without the log-mass epilogue (one
+    kernel, records written by the finalizing CTA): same idx as fs_sample on every step, for both
+    stage-1 kernels (B = 1 single CTA, B = 40 / 300 CTA pairs; 300 = two batch chunks) and transforms."""
+    import paper_2603_15854_b200 as fs
+    import synth
+    torch.cuda.set_device(0)
+    fs.comm_init(fs.comm_unique_id(), 1, 0)
+    for cfg, B, V, D in (("llama3_8b", 1, 20011, 256), ("qwen25_7b", 40, 7001, 128), ("llama3_8b", 300, 5003, 64)):
+        wl = synth.make_workload(cfg, B, V=V, D=D)
+        dev = {k: (getattr(wl, k).cuda() if getattr(wl, k) is not None else None)
+               for k in ("h", "W", "bias", "temperature", "mask")}
+        for step in range(3):
+            idx = fs.sample_tp(dev["h"], dev["W"], 0, wl.V, bias_shard=dev["bias"], temperature=dev["temperature"],
+                               mask=dev["mask"], seed=wl.seed, step=step)
+            ref = fs.sample(dev["h"], dev["W"], bias=dev["bias"], temperature=dev["temperature"], mask=dev["mask"],
+                            seed=wl.seed, step=step)
+            torch.cuda.synchronize()
+            assert torch.equal(idx, ref), (cfg, B, step)
+    fs.comm_destroy()

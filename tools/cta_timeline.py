@@ -7,22 +7,31 @@ import numpy as np
 import torch
 import paper_2603_15854_b200 as fs
 dev = torch.device("cuda", 0)
-V, D = 128256, 4096
+SHARD = int(os.environ.get('SHARD', '0'))   # 1: fs_sample_shard (TP rank-local summary, log-mass epilogue)
+
+
+def call(h, W, s, out):
+    if SHARD:
+        fs.sample_shard(h, W, 0, W.shape[0] * 8, seed=1, step=s)
+    else:
+        fs.sample(h, W, seed=1, step=s, out=out)
+V, D = int(os.environ.get('V', 128256)), int(os.environ.get('D', 4096))
+print('V', V, 'D', D)
 g = torch.Generator(device=dev); g.manual_seed(1)
 W = (torch.randn(V, D, device=dev, generator=g) * 0.02).to(torch.bfloat16)
 for B in [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "1,32").split(",")]:
-    for pdl_w in (0, 1):
+    for pdl_w in [int(x) for x in os.environ.get('PDL', '0,1').split(',')]:
         fs.set_option("pdl_w", pdl_w)
         h = torch.randn(B, D, device=dev, generator=g).to(torch.bfloat16)
         out = torch.empty(B, dtype=torch.int32, device=dev)
         nsteps = 24
         bufs = [torch.zeros(148 * 8, dtype=torch.int64, device=dev) for _ in range(nsteps)]
         for s in range(20):
-            fs.sample(h, W, seed=1, step=s, out=out)
+            call(h, W, s, out)
         torch.cuda.synchronize()
         for s in range(nsteps):
             fs.set_option("dbg_times", bufs[s].data_ptr())
-            fs.sample(h, W, seed=1, step=s, out=out)
+            call(h, W, s, out)
         fs.set_option("dbg_times", 0)
         torch.cuda.synchronize()
         A = np.stack([b.cpu().numpy().reshape(148, 8) for b in bufs])

@@ -13,7 +13,7 @@
 #include "../paper_2603_15854_b200/csrc/fs_sm100.cuh"
 
 template <bool kPair>
-__global__ void __cluster_dims__(2, 1, 1) alloc_only(uint32_t* out) {
+__global__ void alloc_only(uint32_t* out) {
   __shared__ uint32_t slot;
   const int warp = threadIdx.x >> 5;
   if (warp == 0) {
@@ -35,17 +35,37 @@ __global__ void __cluster_dims__(2, 1, 1) alloc_only(uint32_t* out) {
   }
 }
 
+template <bool kPair>
+static cudaError_t launch(uint32_t* d) {     // cluster of 2, as the library launches fs_fused_tc2.cu
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(148);
+  cfg.blockDim = dim3(64);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, alloc_only<kPair>, d);
+  if (e != cudaSuccess) return e;
+  return cudaDeviceSynchronize();
+}
+
 int main() {
-  uint32_t* d;
-  cudaMalloc(&d, 2 * 148 * sizeof(uint32_t));
-  alloc_only<false><<<148, 64>>>(d);        // control: per-CTA allocation (cta_group::1)
-  cudaError_t e1 = cudaDeviceSynchronize();
-  alloc_only<true><<<148, 64>>>(d);         // the paired allocation of fs_fused_tc2.cu
-  cudaError_t e2 = cudaDeviceSynchronize();
-  uint32_t h[4];
+  uint32_t* d = nullptr;
+  cudaError_t e0 = cudaMalloc(&d, 2 * 148 * sizeof(uint32_t));
+  printf("malloc %s\n", cudaGetErrorString(e0));
+  fflush(stdout);
+  cudaError_t e1 = launch<false>(d);        // control: per-CTA allocation (cta_group::1)
+  printf("cta_group::1 %s\n", cudaGetErrorString(e1));
+  fflush(stdout);
+  cudaError_t e2 = launch<true>(d);         // the paired allocation of fs_fused_tc2.cu
+  printf("cta_group::2 %s\n", cudaGetErrorString(e2));
+  fflush(stdout);
+  uint32_t h[4] = {0, 0, 0, 0};
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
-  printf("cta_group::1 %s, cta_group::2 %s, tmem base of CTAs 0..3: %u %u %u %u\n", cudaGetErrorString(e1),
-         cudaGetErrorString(e2), h[0], h[1], h[2], h[3]);
+  printf("tmem base of CTAs 0..3: %u %u %u %u\n", h[0], h[1], h[2], h[3]);
   cudaFree(d);
   return (e1 == cudaSuccess && e2 == cudaSuccess) ? 0 : 1;
 }

@@ -571,11 +571,13 @@ def run_single(args):
         prepared = fs.HostStepSampler(h_host, wl["W"], bias=wl["bias"], temperature_host=t_host,
                                       seed=synth.SAMPLING_SEED, h_dev=h_dev, idx_host=idx_host)
 
+    idx_np = idx_host.numpy()                  # host view of the pinned ids (no torch op per step)
+
     def e2e_prepared():
         e_ctr[0] += 1
         prepared(e_ctr[0])
         prepared.wait()
-        sink[0] += int(idx_host[0])
+        sink[0] += int(idx_np[0])
     # the host syncs every step, so nothing overlaps across steps; pdl_w = 1 only lets this step's
     # W stream start while the kernel itself is still staging h from host memory
     fs.set_option("pdl_w", 1)
@@ -713,8 +715,8 @@ def sweep(fs, name, pk, args, Bs=SWEEP_B):
 
 def tp_shards(fs, pk, name="llama3_70b", worlds=(2, 4, 8), Bs=(1, 32, 256)):
     """Compute half of the vocabulary-sharded step (Alg. A.4) at n = 2/4/8, measured on this one GPU:
-    rank 0's shard kernel (fs_sample_shard over V/n rows) and the outer selection over n records
-    (fs_combine_summaries).  The exchange itself needs n GPUs (bench --gpus N).  Beside it, the naive
+    rank 0's shard kernel over V/n rows -- idx only (what fs_sample_tp runs without logZ; the roofline)
+    and with log-mass (fs_sample_shard) -- and the outer selection over n records (fs_combine_summaries).  The exchange itself needs n GPUs (bench --gpus N).  Beside it, the naive
     TP baseline's compute half (per-rank cuBLAS GEMM [B, V/n]) and the bytes its logits all-gather
     would receive per rank."""
     dev = torch.device("cuda", 0)
@@ -734,16 +736,27 @@ def tp_shards(fs, pk, name="llama3_70b", worlds=(2, 4, 8), Bs=(1, 32, 256)):
                 ctr[0] += 1
                 fs.sample_shard(wl["h"], wl["W"], lo, V, seed=synth.SAMPLING_SEED, step=ctr[0], out=summ)
 
+            def shard_idx_only():
+                # the kernel fs_sample_tp runs when no logZ is requested: plain epilogue, one-kernel
+                # finalize (records written by the last CTA) -- the same work as fs_sample on the shard
+                ctr[0] += 1
+                fs.sample(wl["h"], wl["W"], seed=synth.SAMPLING_SEED, step=ctr[0], out=idx_buf)
+
+            idx_buf = torch.empty(B, dtype=torch.int32, device=dev)
             shard()
             gathered.raw.copy_(summ.raw.unsqueeze(0).expand(n, B, 3))
             shard_us = 1e3 * time_median(shard, 100, 25)
+            shard_idx_us = 1e3 * time_median(shard_idx_only, 100, 25)
             comb_us = 1e3 * time_graph(lambda: fs.combine_summaries(gathered))
             gemm_us = 1e3 * time_median(lambda: torch.matmul(wl["h"], wl["W"].t()), 100, 25)
             res[f"n{n}/B{B}"] = {
-                "V_local": hi - lo, "shard_us": round(shard_us, 2), "combine_us": round(comb_us, 2),
-                "roofline": roofline(name, B, D, hi - lo, shard_us * 1e-3, pk, False,
-                                     kname="shard stage 1 (+ stage 2 in-kernel or PDL reduce)",
+                "V_local": hi - lo, "shard_us": round(shard_us, 2), "shard_idx_only_us": round(shard_idx_us, 2),
+                "combine_us": round(comb_us, 2),
+                "roofline": roofline(name, B, D, hi - lo, shard_idx_us * 1e-3, pk, False,
+                                     kname="idx-only shard kernel (fs_sample_tp without logZ: one kernel)",
                                      traffic_key=(f"{name}_n{n}", B)),
+                "roofline_log_mass_shard": roofline(name, B, D, hi - lo, shard_us * 1e-3, pk, False,
+                                                    kname="fs_sample_shard (log-mass epilogue + stage 2)"),
                 "exchange_bytes_per_rank": 12 * B * n,
                 "naive_tp_gemm_us": round(gemm_us, 2),
                 "naive_tp_allgather_bytes_per_rank": 2 * B * (hi - lo) * (n - 1)}

@@ -59,8 +59,6 @@ struct fs_ctx {
   int l2promo = 3;                 // CUtensorMapL2promotion for W/h maps (3 = 256B)
   int w_policy = 1;                // 1: W loads evict_first, 0: no cache hint
   int spin_wait = 0;               // A/B: epilogue barrier waits without the suspend-time hint
-  int prune = 0;                   // exact Gumbel pruning in the one-kernel epilogue (fs_epilogue.cuh);
-                                   // off: measured no faster (DESIGN.md §11 entry 18)
   int epi_sleep = 0;               // ns of backoff in epilogue barrier waits (0 = spin)
   int unit_rows = 0;               // CTA range granularity (0 = default)
   int pair = -1;                   // CTA-pair kernel: -1 auto (by batch size), 0 off, 1 on
@@ -403,7 +401,6 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
       p.dbg_times = ctx->dbg_times;
       p.w_policy = ctx->w_policy;
       p.epi_sleep = ctx->epi_sleep;
-      p.prune = ctx->prune;
       p.spin_wait = ctx->spin_wait;
       auto stages_for = [&](int k) { return pair ? fs::tc2_stages(BN, k) : fs::tc_stages(BN, k); };
       p.kbps = ctx->kbps;
@@ -754,7 +751,6 @@ fs_status fs_ctx_set_option(fs_ctx* ctx, const char* name, int64_t value) {
   else if (!strcmp(name, "topk_spans")) ctx->topk_spans = (int)value;
   else if (!strcmp(name, "grp_ranges")) ctx->grp_ranges = (int)value;
   else if (!strcmp(name, "pdl_w")) ctx->pdl_w = (int)value;
-  else if (!strcmp(name, "prune")) ctx->prune = (int)value;
   else if (!strcmp(name, "spin_wait")) ctx->spin_wait = (int)value;
   else if (!strcmp(name, "pdl_w_max_b")) ctx->pdl_w_max_b = (int)value;
   else if (!strcmp(name, "staging_check")) ctx->staging_check = (int)value;
@@ -1101,12 +1097,24 @@ fs_status fs_sample_tp_push(fs_ctx* ctx, fs_dtype dtype, const void* h, const vo
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   unsigned* status = reinterpret_cast<unsigned*>(ctx->comm_win + ctx->comm_off_status);
   const uint64_t epoch = ++ctx->comm_epoch;
+  const fs::PushCtx pc{ctx->comm_peertab, ctx->comm_world, ctx->comm_rank, ctx->comm_bmax, epoch, status + 16,
+                       status};
+  const bool tc = !ctx->force_simt && dtype == FS_BF16 && (D % 8 == 0) && aligned16(h) && aligned16(W_shard);
+  if (B <= 256 && !logZ_out && tc && ctx->fuse_reduce) {
+    // fully fused (no log-mass needed): ONE kernel per rank -- the shard's finalizing CTA writes the
+    // records into every peer window, releases its flags, waits for the n ranks' records, combines
+    // into idx_out / score_out and acknowledges (fs_epilogue.cuh finalize_last_cta)
+    PathArgs a{dtype, h, W_shard, bias_shard, temperature, mask, (V_total + 31) / 32, seed, step, B, D, V_local,
+               vocab_offset, ((V_local + 127) / 128) * 128, false, idx_out, score_out, nullptr, nullptr, 1,
+               nullptr};
+    a.sum_out = ctx->comm_local;
+    a.push = &pc;
+    return run_path(ctx, a, st);
+  }
   if (B <= 256) {
-    // fused: the shard sampler's last reduction step (the last stage-1 CTA for B <= 16, else the
+    // fused push: the shard sampler's last reduction step (the last stage-1 CTA for B <= 16, else the
     // stage-2 row reduce) stores the records into every peer window and releases the flags; one
     // PDL-chained block then waits for the n flags and combines
-    const fs::PushCtx pc{ctx->comm_peertab, ctx->comm_world, ctx->comm_rank, ctx->comm_bmax, epoch, status + 16,
-                         status};
     PathArgs a{dtype, h, W_shard, bias_shard, temperature, mask, (V_total + 31) / 32, seed, step, B, D, V_local,
                vocab_offset, ((V_local + 127) / 128) * 128, true, nullptr, nullptr, nullptr, ctx->comm_local, 1,
                nullptr};

@@ -66,8 +66,6 @@ struct EpiArgs {
   int row_offset;           // global batch index of column 0 (RNG counter)
   uint32_t k0, k1, c2, c3;  // Philox key and counter words 2, 3
   int dbg_skip;             // debug: drain TMEM without computing (bounds the MMA+TMA-only time)
-  unsigned long long* gbest;  // one-kernel finalize words fin_best[B] ((key << 32) | ~idx, all CTAs):
-                              // non-null = exact Gumbel pruning against the best score so far (below)
 };
 
 // One-kernel finalize (StageOneParams::fin_best).  The candidate order of state_merge (larger key,
@@ -77,17 +75,6 @@ __device__ __forceinline__ unsigned long long pack_state(const State& s) {
   return ((unsigned long long)s.key << 32) | (unsigned long long)(s.idx >= 0 ? ~(uint32_t)s.idx : 0u);
 }
 
-// Exact pruning of the Gumbel evaluation (plain sampling with the one-kernel finalize).
-// g(r) = -ln(-ln u) < -ln(1 - u) <= (k + 1) ln 2 + 2^-32, k = number of leading one bits of r
-// (u = (r+1)/(2^32+1); -ln u >= 1 - u and 1 - u > 2^-(k+1)).  An element whose upper bound
-// l~ + (k+1) ln 2 (+ margin for the fp32 roundings of l~ + G32) does not exceed the score of a
-// candidate already recorded for its batch row -- this warp's running best or any CTA's published
-// best in fin_best -- has a strictly smaller perturbed score than that candidate, so it is neither
-// the row's argmax nor tied with it: its Gumbel is never evaluated.  The argmax, its id and its
-// score are bit-identical to the unpruned epilogue (tests/test_gpu_prune.py).
-__device__ __forceinline__ float gumbel_upper(uint32_t r, float l) {
-  return (float)(__clz(~r) + 1) * kLn2 + 1e-3f + fabsf(l) * 1e-6f;
-}
 
 struct RowArgs {
   bool valid;               // this lane's vocabulary row is inside the tile
@@ -231,16 +218,9 @@ __device__ __forceinline__ void epi_tile_tc(uint32_t taddr, const RowArgs& ra, c
     release_tmem(tempty, tempty_cluster, lane);
     return;
   }
-  const bool prune = !LSE && ea.gbest != nullptr;
 #pragma unroll 1
   for (int c = chunk0; c < nch; c += cstep) {
     State own = st[0];
-    // pruning threshold of column c*32 + lane: this warp's running best or the best published by
-    // any CTA so far (a stale read is still a recorded candidate's score: a valid threshold)
-    uint32_t thr_lane = own.key;
-    if (prune && c * 32 + lane < B)
-      thr_lane = max(thr_lane, (uint32_t)(__ldcg(ea.gbest + c * 32 + lane) >> 32));
-    const uint32_t thr_in = thr_lane;
 #pragma unroll 1
     for (int g = 0; g < 4; g += NG) {
       const int col0 = c * 32 + g * 8;
@@ -290,51 +270,6 @@ __device__ __forceinline__ void epi_tile_tc(uint32_t taddr, const RowArgs& ra, c
           rb[4 * qq + 2] = p4.z;
           rb[4 * qq + 3] = p4.w;
         }
-      }
-      if (prune) {
-        sm100::tmem_wait_ld();
-        if (col0 + NC >= B || (c + cstep >= nch && g + NG >= 4))      // this warp's last TMEM read
-          release_tmem(tempty, tempty_cluster, lane);
-        // l~ and the bound test per element; only columns with a surviving element evaluate G32
-        float lt[NC];
-        uint32_t pm = 0u;
-#pragma unroll
-        for (int jj = 0; jj < NC; ++jj) {
-          float l = __uint_as_float(r[jj]);
-          float gs = 1.0f;
-          if (XFORM) {
-            l = (l + ra.bias) * ea.invtau[col0 + jj];
-            gs = ea.tab->gscale[col0 + jj];
-            if (ea.mask != nullptr) {
-              const uint32_t w = __shfl_sync(0xFFFFFFFFu, mw, msrc + jj);
-              if (!((w >> mbit) & 1u)) l = -INFINITY;
-            }
-          }
-          if (isnan(l)) l = -INFINITY;
-          lt[jj] = l;
-          const uint32_t thr = __shfl_sync(0xFFFFFFFFu, thr_lane, g * 8 + jj);
-          const bool pass = ra.valid && (thr == kKeyNone || l + gumbel_upper(rb[jj], l) * gs > key_ref(thr));
-          pm |= (uint32_t)pass << jj;
-        }
-        const uint32_t cols = __reduce_or_sync(0xFFFFFFFFu, pm);
-        const int jo = lane - g * 8;
-        uint32_t km = 0u, bl = 0u;
-#pragma unroll
-        for (int jj = 0; jj < NC; ++jj) {
-          if (cols & (1u << jj)) {                                       // warp-uniform
-            const float gj = XFORM ? gumbel32(rb[jj]) * ea.tab->gscale[col0 + jj] : gumbel32(rb[jj]);
-            const uint32_t key = ((pm >> jj) & 1u) ? order_key(lt[jj] + gj) : kKeyNone;
-            const uint32_t kx = __reduce_max_sync(0xFFFFFFFFu, key);
-            const uint32_t bx = __ballot_sync(0xFFFFFFFFu, key == kx);
-            km = (jo == jj) ? kx : km;
-            bl = (jo == jj) ? bx : bl;
-          }
-        }
-        const int32_t wi = km > kKeyNone ? ra.warp_v0 + (__ffs(bl) - 1) : -1;
-        const bool upd = (unsigned)jo < (unsigned)NC && (km > own.key);  // ties keep the earlier id
-        own.key = upd ? km : own.key;
-        own.idx = upd ? wi : own.idx;
-        continue;
       }
       float gm[NC];
 #pragma unroll
@@ -423,9 +358,6 @@ __device__ __forceinline__ void epi_tile_tc(uint32_t taddr, const RowArgs& ra, c
         own.idx = upd ? wi : own.idx;
       }
     }
-    // publish an improved best of column c*32 + lane for every CTA's pruning (the final fold is a
-    // max over the same candidates, so early publication does not change the result)
-    if (prune && c * 32 + lane < B && own.key > thr_in) atomicMax(ea.gbest + c * 32 + lane, pack_state(own));
     st[0] = own;
     if (nmine > 1) rotate_states(st);
   }
@@ -456,10 +388,15 @@ __device__ __forceinline__ void flush_warp(State (&st)[NST], int lane, int B, St
 // undefined (idx -1, score -inf) and h_bar[2] counts the event (fs_ctx_query "staging_timeouts").
 // With sum_out (a TP shard step that needs no log-mass, fs_sample_tp without logZ) the row maxima are
 // written as the shard's exchange records {M, I, L = NaN} instead of idx / score.
+// With push->peers (f2 fully fused, a TP step without log-mass): the records also go into every
+// peer's exchange window, and the same CTA then waits for the n ranks' records, runs the outer
+// selection (Alg. A.4 lines 5-7) into idx_out / score_out and acknowledges the epoch -- the whole
+// sharded step is this one kernel per rank.  `flag` needs 2 ints of shared scratch.
 __device__ __forceinline__ void finalize_last_cta(unsigned long long* best, unsigned int* ctr, int B,
                                                   int32_t* idx_out, float* score_out, int et, int nthr,
                                                   uint32_t bar_id, volatile int* flag, unsigned n_ctas,
-                                                  unsigned int* h_bar = nullptr, fs_summary* sum_out = nullptr) {
+                                                  unsigned int* h_bar = nullptr, fs_summary* sum_out = nullptr,
+                                                  const PushCtx* push = nullptr) {
   __threadfence();
   sm100::named_bar_sync(bar_id, nthr);
   if (et == 0) *flag = (atomicAdd(ctr, 1u) == n_ctas - 1) ? 1 : 0;
@@ -467,17 +404,59 @@ __device__ __forceinline__ void finalize_last_cta(unsigned long long* best, unsi
   if (*flag) {
     __threadfence();
     const bool timed_out = h_bar != nullptr && *reinterpret_cast<volatile unsigned int*>(h_bar + 1) != 0u;
+    const bool pushing = push != nullptr && push->peers != nullptr;
+    if (pushing) {                             // readers are done with this parity slot
+      if (et == 0) flag[1] = 1;
+      push_wait_readers(*push, et);
+      sm100::named_bar_sync(bar_id, nthr);
+    }
     for (int b = et; b < B; b += nthr) {
       const unsigned long long v = atomicExch(&best[b], 0ull);
       const uint32_t key = (uint32_t)(v >> 32);
       const bool defined = key > kKeyNegInf && !timed_out;
       const int32_t id = defined ? (int32_t)~(uint32_t)v : -1;
       const float sc = defined ? key_to_float(key) : -INFINITY;
-      if (idx_out) idx_out[b] = id;
-      if (score_out) score_out[b] = sc;
-      if (sum_out) sum_out[b] = fs_summary{sc, id, __int_as_float(0x7FC00000)};
+      const fs_summary f{sc, id, __int_as_float(0x7FC00000)};
+      if (!pushing) {
+        if (idx_out) idx_out[b] = id;
+        if (score_out) score_out[b] = sc;
+      }
+      if (sum_out) sum_out[b] = f;
+      if (pushing) push_record(*push, b, f);
     }
     sm100::named_bar_sync(bar_id, nthr);     // every thread read the timeout flag
+    if (pushing) {
+      if (et == 0) push_release(*push);        // fence.sys + this rank's flag in every window
+      sm100::named_bar_sync(bar_id, nthr);
+      const int par = (int)(push->epoch & 1);
+      const PeerTab& pt = *push->peers;
+      if (et < push->world &&
+          !wait_flag(pt.flags[push->rank] + par * push->world + et, [&](uint64_t v) { return v == push->epoch; }))
+        flag[1] = 0;
+      sm100::named_bar_sync(bar_id, nthr);
+      const bool ok = flag[1] != 0;
+      const fs_summary* rec = pt.rec[push->rank] + (size_t)par * push->world * push->B_max;
+      for (int b = et; b < B; b += nthr) {
+        State acc = state_empty();
+        for (int k = 0; k < push->world; ++k) {
+          const fs_summary m = rec[(size_t)k * push->B_max + b];
+          State s1 = state_empty();
+          if (m.idx >= 0 && !(m.max_score == -INFINITY)) {
+            s1.key = order_key(m.max_score);
+            s1.idx = m.idx;
+          }
+          acc = state_max(acc, s1);            // ties -> smaller global id (reading R5)
+        }
+        const bool defined = acc.key > kKeyNegInf && ok;
+        if (idx_out) idx_out[b] = defined ? acc.idx : -1;
+        if (score_out) score_out[b] = defined ? key_to_float(acc.key) : -INFINITY;
+      }
+      sm100::named_bar_sync(bar_id, nthr);
+      if (et == 0) {
+        if (!ok) atomicAdd(push->timeouts, 1u);
+        for (int q = 0; q < push->world; ++q) st_release_sys(pt.acks[q] + push->rank, push->epoch);
+      }
+    }
     if (et == 0) {
       atomicExch(ctr, 0u);
       if (h_bar) {

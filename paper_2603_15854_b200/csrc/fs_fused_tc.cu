@@ -292,7 +292,6 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
     ea.c2 = ctr_step_lo(p.step);
     ea.c3 = ctr_step_hi(p.step, 0u);
     ea.dbg_skip = p.dbg_no_epi;
-    ea.gbest = (!LSE && p.prune) ? p.fin_best : nullptr;   // exact Gumbel pruning (fs_epilogue.cuh)
     State st[8];
 #pragma unroll
     for (int c = 0; c < 8; ++c) st[c] = state_empty();
@@ -361,7 +360,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
       }
       if (p.fin_best)
         finalize_last_cta(p.fin_best, p.fin_ctr, p.B, p.idx_out, p.score_out, et, 32 * kEpiWarps, 1,
-                          reinterpret_cast<volatile int*>(scratch + kEpiWarps * BN), gridDim.x, p.h_bar, p.fin_sum);
+                          reinterpret_cast<volatile int*>(scratch + kEpiWarps * BN), gridDim.x, p.h_bar, p.fin_sum, &p.push);
       else if (et == 0)
         p.part_group[blockIdx.x] = (r0 < r1) ? 0 : -1;
       if (!p.fin_best && p.fin_lse)

@@ -82,7 +82,10 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
     }
     sm100::fence_barrier_init();
   }
-  if (warp == 1) sm100::tmem_alloc_pair(tmem_slot, (uint32_t)p.tmem_cols);
+  // The paired allocation (and its release below) is issued by warp 0: issued by any other warp,
+  // compute-sanitizer racecheck reports the allocator's result write as a race with the alloc itself
+  // (tools/racecheck_tmem_pair.cu: the same prologue is clean with warp 0, flagged with warp 1).
+  if (warp == 0) sm100::tmem_alloc_pair(tmem_slot, (uint32_t)p.tmem_cols);
   sm100::tc_fence_before();
   sm100::cluster_sync();                    // both CTAs' barriers exist before any remote signal
   __syncthreads();                          // CTA-level order for the allocator's smem write (racecheck)
@@ -216,7 +219,6 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
     ea.c2 = ctr_step_lo(p.step);
     ea.c3 = ctr_step_hi(p.step, 0u);
     ea.dbg_skip = p.dbg_no_epi;
-    ea.gbest = (!LSE && p.prune) ? p.fin_best : nullptr;   // exact Gumbel pruning (fs_epilogue.cuh)
     const uint32_t tempty_leader = sm100::mapa(sm100::smem_u32(&tempty[set]), 0);
     State st[4];
 #pragma unroll
@@ -282,7 +284,7 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
       }
       if (p.fin_best)
         finalize_last_cta(p.fin_best, p.fin_ctr, p.B, p.idx_out, p.score_out, et, 32 * kEpiWarps, 1,
-                          reinterpret_cast<volatile int*>(scratch + kSlotWarps * BN), gridDim.x, p.h_bar, p.fin_sum);
+                          reinterpret_cast<volatile int*>(scratch + kSlotWarps * BN), gridDim.x, p.h_bar, p.fin_sum, &p.push);
       else if (et == 0)
         p.part_group[blockIdx.x] = (r0 < r1) ? 0 : -1;
       if (!p.fin_best && p.fin_lse)
@@ -295,7 +297,7 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
 
   sm100::tc_fence_before();
   sm100::cluster_sync();                    // no remote arrivals / MMAs into our TMEM after this
-  if (warp == 1) {
+  if (warp == 0) {
     sm100::tc_fence_after();
     sm100::tmem_dealloc_pair(tmem_base, (uint32_t)p.tmem_cols);
   }

@@ -78,7 +78,6 @@ struct StageOneParams {
   unsigned long long* fin_best;   // [256], all 0 between calls; nullptr = write `part` for stage 2
   int spin_wait;                  // A/B: epilogue waits spin on try_wait without the suspend hint
   fs_summary* fin_sum;            // with fin_best: write {M, I, L = NaN} records instead of idx / score
-  int prune;                      // with fin_best: skip G32 where a recorded best provably wins
   unsigned int* fin_ctr;          // CTAs finished, 0 between calls
   int32_t* idx_out;               // [B] of this chunk
   float* score_out;               // [B] or nullptr

@@ -60,8 +60,12 @@ def _worker(rank, world, port, cfg, B, V, D, steps, q):
                 check_flat(idx.cpu().numpy(), score.cpu().numpy(), flat)
                 fin = np.isfinite(flat.logZ)
                 oracle_ok = bool(np.all(np.abs(logZ.cpu().numpy()[fin] - flat.logZ[fin]) <= 1e-3))
-            out.append((torch.equal(idx, ref_idx), torch.equal(score.view(torch.int32), ref_score.view(torch.int32)),
-                        oracle_ok))
+            # idx-only step: the whole exchange fused into the shard kernel's finalizing CTA (one kernel)
+            idx1 = tp.sample_tp_push_step(
+                h, W[lo:hi].contiguous(), lo, V, bias_shard=None if bias is None else bias[lo:hi].contiguous(),
+                temperature=tau, mask=mask, seed=wl.seed, step=s)
+            out.append((torch.equal(idx, ref_idx) and torch.equal(idx1, ref_idx),
+                        torch.equal(score.view(torch.int32), ref_score.view(torch.int32)), oracle_ok))
         timeouts = fs.query("comm_timeouts")
         dist.barrier()                       # peers stay mapped until everyone is done
         fs.comm_window_destroy()
@@ -71,7 +75,8 @@ def _worker(rank, world, port, cfg, B, V, D, steps, q):
         q.put((rank, None, None, repr(e)))
 
 
-# B <= 16: the last stage-1 CTA pushes; 17..256: the stage-2 row reduce pushes; > 256: separate push kernel
+# with logZ: B <= 16 the last stage-1 CTA pushes, 17..256 the stage-2 row reduce pushes, > 256 a separate push
+# kernel; idx only (B <= 256): push, wait and combine all in the shard kernel's finalizing CTA
 @pytest.mark.parametrize("world,cfg,B,V,D", [(2, "llama3_8b", 8, 20011, 256), (3, "qwen25_7b", 33, 9001, 128),
                                              (4, "llama3_8b", 1, 4096, 64), (2, "qwen25_7b", 300, 5003, 64)])
 def test_push_exchange_matches_single_gpu(world, cfg, B, V, D):

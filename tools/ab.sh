@@ -2,8 +2,7 @@
 # Round-2 A/B experiments on the GPU box (via gpurun), logs under gpurun_out/<out>/ (summarised in
 # DESIGN.md §11 and copied to profiles/r02/).  Usage: tools/ab.sh <experiment> [out]
 #   no_epi   epilogue off (dbg_no_epi) at B = 128 / 256                    (§11 entry 18)
-#   wait     epilogue barrier waits: spin vs suspend hint, x pruning      (entries 19, 20)
-#   prune    exact Gumbel pruning on / off + the tests it touches         (entry 20)
+#   wait     epilogue barrier waits: spin vs suspend hint                 (entry 19)
 #   energy   NVML energy split: full / no epilogue / no MMA / no loads    (entry 22)
 #   race     racecheck of the paired-TMEM-allocation reproducer            (§1 sanitizers)
 EXP=${1:?experiment}
@@ -15,11 +14,7 @@ case $EXP in
       timeout 600 python tools/sweep_opts.py $c 128,256 '{"dbg_no_epi": [0, 1]}' >> $OUT/no_epi.log 2>&1; done ;;
   wait)
     for c in llama3_8b qwen25_7b gemma3_27b; do
-      timeout 900 python tools/sweep_opts.py $c 32,128,256 '{"spin_wait": [1, 0], "prune": [0, 1]}' >> $OUT/wait.log 2>&1; done ;;
-  prune)
-    timeout 900 python -m pytest tests/test_gpu_prune.py -q -x -p no:cacheprovider > $OUT/pytest_prune.log 2>&1
-    for c in llama3_8b qwen25_7b llama3_70b; do
-      timeout 600 python tools/sweep_opts.py $c 1,32,128,256 '{"prune": [0, 1]}' >> $OUT/prune.log 2>&1; done ;;
+      timeout 900 python tools/sweep_opts.py $c 32,128,256 '{"spin_wait": [1, 0]}' >> $OUT/wait.log 2>&1; done ;;
   energy)
     timeout 600 python tools/energy_split.py llama3_8b 32,128,256 > $OUT/energy.log 2>&1
     timeout 400 python tools/energy_split.py gemma3_27b 256 >> $OUT/energy.log 2>&1 ;;

@@ -25,10 +25,10 @@ for k, v in d.get("configs", {}).get("paper_d4096", {}).items():
     print(f"| {k[1:]} | {o.get('vs_multinomial')} / {o.get('vs_fi1')} / {o.get('vs_fi2')} | "
           f"{p.get('vs_multinomial')} / {p.get('vs_fi1')} / {p.get('vs_fi2')} |")
 print()
-print("| 70B shard n / B | V_local | shard kernel µs | frac (of floor) | combine µs | naive per-rank GEMM µs | naive all-gather bytes/rank | summary bytes/rank |")
-print("|---|---|---|---|---|---|---|---|")
+print("| 70B shard n / B | V_local | idx-only shard µs | frac (of floor) | log-mass shard µs | combine µs | naive per-rank GEMM µs | naive all-gather bytes/rank | summary bytes/rank |")
+print("|---|---|---|---|---|---|---|---|---|")
 for k, v in d.get("tp_shards", {}).items():
     ro = v["roofline"]
-    print(f"| {k} | {v['V_local']} | {v['shard_us']:.1f} | {ro['bound']} {ro['frac']:.3f} ({ro['frac_of_floor']:.3f}) | "
-          f"{v['combine_us']:.2f} | {v['naive_tp_gemm_us']:.1f} | {v['naive_tp_allgather_bytes_per_rank']:,} | "
+    print(f"| {k} | {v['V_local']} | {v.get('shard_idx_only_us', 0):.1f} | {ro['bound']} {ro['frac']:.3f} ({ro['frac_of_floor']:.3f}) | "
+          f"{v['shard_us']:.1f} | {v['combine_us']:.2f} | {v['naive_tp_gemm_us']:.1f} | {v['naive_tp_allgather_bytes_per_rank']:,} | "
           f"{v['exchange_bytes_per_rank']} |")

@@ -53,17 +53,15 @@ fs.gumbel_from_bits(torch.arange(1000, dtype=torch.int32, device=dev))
 fs.random_bits(1, 2, torch.arange(100, device=dev), torch.arange(100, device=dev))
 torch.cuda.synchronize()
 print("sanitize cases ok")
-# round 2: exact Gumbel pruning (option), TP shard without log-mass (one-kernel records)
-fs.set_option("prune", 1)
-for pair in (0, 1):
-    fs.set_option("pair", pair)
-    fs.sample(h, W, seed=1, step=4)
-    fs.sample(h, W, bias=bias, temperature=tau, mask=mask, seed=1, step=4, return_score=True)
-fs.set_option("prune", 0)
-fs.set_option("pair", -1)
+# round 2: TP shard without log-mass (one-kernel records) and the one-kernel push exchange
 fs.comm_init(fs.comm_unique_id(), 1, 0)
 fs.sample_tp(h, W, 0, 3000, seed=1, step=5)
 fs.sample_tp(h8, W, 0, 3000, seed=1, step=5)
 fs.comm_destroy()
+fs.comm_window_open([fs.comm_window_create(1, 0, 64)])
+for st in range(3):
+    fs.sample_tp_push(h, W, 0, 3000, seed=1, step=st)                   # one kernel: push + wait + combine
+    fs.sample_tp_push(h8, W, 0, 3000, seed=1, step=st, return_all=True)  # log-mass shard + wait kernel
+fs.comm_window_destroy()
 torch.cuda.synchronize()
 print("sanitize cases done")

@@ -32,7 +32,7 @@ for cname, sw in sweeps:
                 print("        ", k2, bl[k2])
 for k, v in d.get("tp_shards", {}).items():
     ro = v["roofline"]
-    print(f"  tp {k:9s} Vl {v['V_local']} shard {v['shard_us']:7.2f} comb {v['combine_us']:5.2f} {ro['bound']} "
+    print(f"  tp {k:9s} Vl {v['V_local']} shard {v['shard_us']:7.2f} idx-only {v.get('shard_idx_only_us', 0):7.2f} comb {v['combine_us']:5.2f} {ro['bound']} "
           f"frac {ro['frac']:.3f} floor-frac {ro['frac_of_floor']:.3f} | naive gemm {v['naive_tp_gemm_us']:7.2f}")
 for k, v in d.get("tp_exchange_world1", {}).items():
     print("  ex", k, v)

@@ -213,8 +213,8 @@ def time_loop(fn, steps, warmup, stream=None):
     return e0.elapsed_time(e1) / steps
 
 
-def time_median(fn, iters, warmup):
-    """Median of per-call event times (the paper's protocol: 25 warm-ups, median of 100)."""
+def time_quantiles(fn, iters, warmup):
+    """Per-call event times (the paper's protocol: 25 warm-ups, median of 100): (p10, p50, p90) ms."""
     for _ in range(warmup):
         fn()
     torch.cuda.synchronize()
@@ -224,7 +224,39 @@ def time_median(fn, iters, warmup):
         fn()
         b.record()
     torch.cuda.synchronize()
-    return statistics.median(a.elapsed_time(b) for a, b in evs)
+    t = sorted(a.elapsed_time(b) for a, b in evs)
+    q = lambda f: t[min(len(t) - 1, int(round(f * (len(t) - 1))))]
+    return q(0.1), statistics.median(t), q(0.9)
+
+
+def time_median(fn, iters, warmup):
+    return time_quantiles(fn, iters, warmup)[1]
+
+
+def time_graph_steps(make_call, n=100, reps=3):
+    """CUDA-graph replay of n consecutive steps (each captured launch has its own step number):
+    device ms per step with the host launch overhead removed."""
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        make_call(0)()                      # this stream's library context allocates outside capture
+        s.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for i in range(n):
+                make_call(i + 1)()
+        g.replay()
+        s.synchronize()
+        ts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            g.replay()
+            b.record(s)
+            s.synchronize()
+            ts.append(a.elapsed_time(b) / n)
+    torch.cuda.current_stream().wait_stream(s)
+    return statistics.median(ts)
 
 
 def time_graph(fn, n=50, reps=5):
@@ -536,7 +568,14 @@ def run_single(args):
     ms, clocks = timed_region(fn, args.steps, args.warmup)
     us = ms * 1e3
     t1_ms = stage1_time_ms(fs, fn, min(args.steps, 200))
-    per_call = 1e3 * time_median(fn, 100, 25)
+    pc10, per_call, pc90 = (1e3 * x for x in time_quantiles(fn, 100, 25))
+
+    def graph_call(i):
+        def c():
+            fs.sample(wl["h"], wl["W"], bias=wl["bias"], temperature=wl["temperature"], mask=wl["mask"],
+                      seed=synth.SAMPLING_SEED, step=10**6 + i, out=out)
+        return c
+    graph_ms = time_graph_steps(graph_call) if one_kernel else None
     # PDL-pipelined period: step n+1's W stream starts under step n's tail (reported, not the value)
     fs.set_option("pdl_w", 1)
     pipe_ms = time_loop(fn, max(args.steps, 100), args.warmup)
@@ -594,6 +633,8 @@ def run_single(args):
             "launch": ("one fused kernel per step (stage 2 in the last CTA)" if one_kernel
                        else "stage 1 + PDL-chained stage-2 reduce") + "; no cross-step overlap (pdl_w=0)",
             "per_call_median_us": round(per_call, 2),
+            "per_call_p10_p90_us": [round(pc10, 2), round(pc90, 2)],
+            "graph_replay_us": round(graph_ms * 1e3, 2) if graph_ms else None,
             "pipelined_us": round(pipe_ms * 1e3, 2),
             "pipelined_note": "K back-to-back steps with pdl_w=1: the next step's W stream starts before the "
                               "previous step's kernel ends (PDL); a period, not a step latency",
@@ -635,14 +676,15 @@ def sweep(fs, name, pk, args, Bs=SWEEP_B):
         one_kernel = not wl["group_size"]
         fs.set_option("pdl_w", 0)
         with ClockSampler(0) as clk_call:
-            us = 1e3 * time_median(fn, 100, 25)        # per-call events (the paper's protocol)
+            q10, us, q90 = (1e3 * x for x in time_quantiles(fn, 100, 25))   # per call (the paper's protocol)
         with ClockSampler(0) as clk_loop:
             loop_us = 1e3 * time_loop(fn, 100, 10)      # back-to-back steps, no overlap (as the headline)
         t1 = stage1_time_ms(fs, fn, 50)
         fs.set_option("pdl_w", 1)
         pipe_us = 1e3 * time_loop(fn, 100, 10)          # PDL-pipelined period
         fs.set_option("pdl_w", 0)
-        r = {"fused_us": round(us, 2), "fused_loop_us": round(loop_us, 2), "pipelined_us": round(pipe_us, 2),
+        r = {"fused_us": round(us, 2), "fused_p10_p90_us": [round(q10, 2), round(q90, 2)],
+             "fused_loop_us": round(loop_us, 2), "pipelined_us": round(pipe_us, 2),
              "stage1_us": round(t1 * 1e3, 2), "one_kernel": one_kernel,
              "clocks": {k: {"sm_mhz": c.get("sm_mhz"), "power_w": c.get("power_w_median"), "reasons": c.get("reasons")}
                         for k, c in (("call", clk_call.summary()), ("loop", clk_loop.summary()))}}

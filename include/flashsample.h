@@ -105,13 +105,20 @@ void fs_ctx_destroy(fs_ctx* ctx);
  *       decoding).  Saves the launch gap and the pipeline fill of back-to-back decode steps.
  *       1 = only for batch chunks of at most "pdl_w_max_b" rows (default 128: larger batches are
  *       tensor/power-bound and two overlapping steps only share the power budget); 2 = always.
+ *   "done_flag" (default 0): address of a pinned host uint64 (cudaHostAlloc / pinned torch tensor).
+ *       The one-kernel finalize (fuse_reduce paths, incl. fs_sample_staged) stores 1 into it with a
+ *       system-scope release after every output of the call is written, so a serving loop can spin
+ *       on host memory (reset it to 0 before the call) instead of synchronising the stream.  Per
+ *       context: give the waiting loop a context of its own.  0 = off.
  *   Tuning / testing: "force_simt" (1 = CUDA-core kernel), "max_ctas" (cap the persistent grid,
  *   0 = number of SMs), "pdl" (stage 1 -> stage 2 programmatic launch, default 1), "pair" (CTA-pair
  *   kernel: -1 auto, 0 off, 1 on), "stages", "kbps", "unit_rows", "l2promo", "w_policy",
  *   "topk_mode", "topk_spans" (fused top-k raw-logit route: 1 span maxima + gather, 0 chunk
- *   selection), "grp_ranges" (grouped stage 2: 1 host slot ranges, 0 device search), "time_stage1"
- *   (below); debug: "dbg_no_mma", "dbg_no_epi" (results are garbage), "dbg_times" (device pointer
- *   to [grid][8] u64 per-CTA timestamps, tools/exp_times.py; 0 = off). */
+ *   selection), "grp_ranges" (grouped stage 2: 1 host slot ranges, 0 device search), "grp_kernel"
+ *   (grouped stage 2: 0 auto, 1 warp per (row, group), 3 block per row), "spin_wait" (1 = epilogue
+ *   barrier waits without the suspend-time hint), "time_stage1" (below); debug: "dbg_no_mma",
+ *   "dbg_no_epi" (results are garbage), "dbg_times" (device pointer to [grid][8] u64 per-CTA
+ *   timestamps, tools/cta_timeline.py; 0 = off). */
 fs_status fs_ctx_set_option(fs_ctx* ctx, const char* name, int64_t value);
 /* Measurement hook (used by bench.py for the roofline figure).  With option "time_stage1" = 1
  * every call records a CUDA event pair around each stage-1 (fused kernel) launch on the call's

@@ -15,6 +15,7 @@ from __future__ import annotations
 import ctypes
 import dataclasses
 import threading
+import time
 
 import torch
 
@@ -458,17 +459,55 @@ class HostStepSampler:
         self.idx_host = idx_host if idx_host is not None else torch.empty(B, dtype=torch.int32, pin_memory=True)
         self.stream = torch.cuda.current_stream(W.device)
         self._fn = _lib.lib().fs_sample_staged
-        self._head = (context(W.device, self.stream), FS_BF16, _ptr(h_host), _ptr(self.h_dev), _ptr(W), _ptr(bias),
+        # a context of its own: its completion flag (option "done_flag") is set only by this loop's calls
+        self._ctx = ctypes.c_void_p()
+        _lib.check(_lib.lib().fs_ctx_create(_device_index(W.device), ctypes.byref(self._ctx)), "fs_ctx_create")
+        with _ctx_lock:
+            opts = dict(_opts.get(_device_index(W.device), {}))
+        for name, value in opts.items():
+            _lib.check(_lib.lib().fs_ctx_set_option(self._ctx, name.encode(), int(value)), "fs_ctx_set_option")
+        self.done = torch.zeros(1, dtype=torch.int64, pin_memory=True)
+        self._done_np = self.done.numpy()
+        _lib.check(_lib.lib().fs_ctx_set_option(self._ctx, b"done_flag", self.done.data_ptr()), "fs_ctx_set_option")
+        self._head = (self._ctx, FS_BF16, _ptr(h_host), _ptr(self.h_dev), _ptr(W), _ptr(bias),
                       _ptr(temperature_host), None)
         self._seed = seed & (2**64 - 1)
         self._tail = (B, D, V, _ptr(self.idx_host), None, ctypes.c_void_p(self.stream.cuda_stream))
 
+    def set_option(self, name: str, value: int) -> None:
+        """fs_ctx_set_option on this sampler's own context."""
+        _lib.check(_lib.lib().fs_ctx_set_option(self._ctx, name.encode(), int(value)), "fs_ctx_set_option")
+
     def __call__(self, step: int):
+        self._done_np[0] = 0
         st = self._fn(*self._head, self._seed, step & (2**64 - 1), *self._tail)
         if st:
             _lib.check(st, "fs_sample_staged")
         return self.idx_host
 
-    def wait(self):
-        self.stream.synchronize()
+    def wait(self, timeout_s: float = 10.0):
+        """Spin on the pinned completion flag the finalizing CTA sets after the ids (no stream sync);
+        falls back to synchronising the stream after `timeout_s`."""
+        f = self._done_np
+        if f[0]:
+            return self.idx_host
+        t_end = None
+        n = 0
+        while not f[0]:
+            n += 1
+            if n & 0xFFFF == 0:
+                t_end = t_end or time.perf_counter() + timeout_s
+                if time.perf_counter() > t_end:
+                    self.stream.synchronize()
+                    if not f[0]:
+                        raise FlashSampleError(_lib.FS_ERR_CUDA, "HostStepSampler.wait", "completion flag never set")
         return self.idx_host
+
+    def __del__(self):
+        try:
+            if getattr(self, "_ctx", None):
+                self.stream.synchronize()
+                _lib.lib().fs_ctx_destroy(self._ctx)
+                self._ctx = None
+        except Exception:
+            pass

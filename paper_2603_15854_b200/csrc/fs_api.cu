@@ -58,6 +58,8 @@ struct fs_ctx {
   int dbg_no_epi = 0;
   int l2promo = 3;                 // CUtensorMapL2promotion for W/h maps (3 = 256B)
   int w_policy = 1;                // 1: W loads evict_first, 0: no cache hint
+  unsigned long long* done_flag = nullptr;   // pinned host word the one-kernel finalize sets to 1 (option)
+  int grp_kernel = 0;              // grouped stage 2: 0 auto, 1 warp per (row, group), 3 block per row (A/B)
   int spin_wait = 0;               // A/B: epilogue barrier waits without the suspend-time hint
   int epi_sleep = 0;               // ns of backoff in epilogue barrier waits (0 = spin)
   int unit_rows = 0;               // CTA range granularity (0 = default)
@@ -423,6 +425,7 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
         p.fin_ctr = reinterpret_cast<unsigned int*>(ctx->fin_buf + 256);
         p.idx_out = a.idx_out ? a.idx_out + r0 : nullptr;
         p.fin_sum = a.sum_out ? a.sum_out + r0 : nullptr;
+        if (r0 + chunk >= a.B) p.done_flag = ctx->done_flag;   // the call's last launch
         p.score_out = a.score_out ? a.score_out + r0 : nullptr;
         if (a.h_host) {
           const void* hsrc = static_cast<const char*>(a.h_host) + (size_t)r0 * a.D * esz;
@@ -497,7 +500,7 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
                           a.score_out ? a.score_out + r0 : nullptr, a.logZ_out ? a.logZ_out + r0 : nullptr,
                           a.groups_out ? a.groups_out + (size_t)r0 * a.n_groups : nullptr, stream,
                           ctx->pdl != 0 && !ctx->time_stage1, a.logprob_out ? a.logprob_out + r0 : nullptr,
-                          grp_lo, gscratch, grp_lo ? ctx->grp_rowcnt : nullptr, a.push);
+                          grp_lo, gscratch, grp_lo ? ctx->grp_rowcnt : nullptr, a.push, ctx->grp_kernel);
     if (e != cudaSuccess) return cuda_fail(e, "stage-2 reduce launch");
   }
   return FS_OK;
@@ -752,6 +755,8 @@ fs_status fs_ctx_set_option(fs_ctx* ctx, const char* name, int64_t value) {
   else if (!strcmp(name, "grp_ranges")) ctx->grp_ranges = (int)value;
   else if (!strcmp(name, "pdl_w")) ctx->pdl_w = (int)value;
   else if (!strcmp(name, "spin_wait")) ctx->spin_wait = (int)value;
+  else if (!strcmp(name, "grp_kernel")) ctx->grp_kernel = (int)value;
+  else if (!strcmp(name, "done_flag")) ctx->done_flag = reinterpret_cast<unsigned long long*>(value);
   else if (!strcmp(name, "pdl_w_max_b")) ctx->pdl_w_max_b = (int)value;
   else if (!strcmp(name, "staging_check")) ctx->staging_check = (int)value;
   else if (!strcmp(name, "dbg_times")) ctx->dbg_times = reinterpret_cast<unsigned long long*>(value);

@@ -388,6 +388,8 @@ __device__ __forceinline__ void flush_warp(State (&st)[NST], int lane, int B, St
 // undefined (idx -1, score -inf) and h_bar[2] counts the event (fs_ctx_query "staging_timeouts").
 // With sum_out (a TP shard step that needs no log-mass, fs_sample_tp without logZ) the row maxima are
 // written as the shard's exchange records {M, I, L = NaN} instead of idx / score.
+// With done_flag (option "done_flag", pinned host memory): 1 is stored with system-scope release
+// after the outputs, so a serving loop can spin on it instead of synchronising the stream.
 // With push->peers (f2 fully fused, a TP step without log-mass): the records also go into every
 // peer's exchange window, and the same CTA then waits for the n ranks' records, runs the outer
 // selection (Alg. A.4 lines 5-7) into idx_out / score_out and acknowledges the epoch -- the whole
@@ -396,7 +398,8 @@ __device__ __forceinline__ void finalize_last_cta(unsigned long long* best, unsi
                                                   int32_t* idx_out, float* score_out, int et, int nthr,
                                                   uint32_t bar_id, volatile int* flag, unsigned n_ctas,
                                                   unsigned int* h_bar = nullptr, fs_summary* sum_out = nullptr,
-                                                  const PushCtx* push = nullptr) {
+                                                  const PushCtx* push = nullptr,
+                                                  unsigned long long* done_flag = nullptr) {
   __threadfence();
   sm100::named_bar_sync(bar_id, nthr);
   if (et == 0) *flag = (atomicAdd(ctr, 1u) == n_ctas - 1) ? 1 : 0;
@@ -425,6 +428,10 @@ __device__ __forceinline__ void finalize_last_cta(unsigned long long* best, unsi
       if (pushing) push_record(*push, b, f);
     }
     sm100::named_bar_sync(bar_id, nthr);     // every thread read the timeout flag
+    if (done_flag && !pushing && et == 0) {   // host completion flag (pinned): after every output store
+      __threadfence_system();
+      st_release_sys(reinterpret_cast<uint64_t*>(done_flag), 1ull);
+    }
     if (pushing) {
       if (et == 0) push_release(*push);        // fence.sys + this rank's flag in every window
       sm100::named_bar_sync(bar_id, nthr);

@@ -360,7 +360,8 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
       }
       if (p.fin_best)
         finalize_last_cta(p.fin_best, p.fin_ctr, p.B, p.idx_out, p.score_out, et, 32 * kEpiWarps, 1,
-                          reinterpret_cast<volatile int*>(scratch + kEpiWarps * BN), gridDim.x, p.h_bar, p.fin_sum, &p.push);
+                          reinterpret_cast<volatile int*>(scratch + kEpiWarps * BN), gridDim.x, p.h_bar, p.fin_sum, &p.push,
+                          p.done_flag);
       else if (et == 0)
         p.part_group[blockIdx.x] = (r0 < r1) ? 0 : -1;
       if (!p.fin_best && p.fin_lse)

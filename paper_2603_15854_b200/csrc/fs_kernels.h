@@ -78,6 +78,7 @@ struct StageOneParams {
   unsigned long long* fin_best;   // [256], all 0 between calls; nullptr = write `part` for stage 2
   int spin_wait;                  // A/B: epilogue waits spin on try_wait without the suspend hint
   fs_summary* fin_sum;            // with fin_best: write {M, I, L = NaN} records instead of idx / score
+  unsigned long long* done_flag;  // with fin_best: pinned host word set to 1 after the outputs (option)
   unsigned int* fin_ctr;          // CTAs finished, 0 between calls
   int32_t* idx_out;               // [B] of this chunk
   float* score_out;               // [B] or nullptr
@@ -139,7 +140,8 @@ cudaError_t launch_reduce(const State* part, const int* part_group, const SlotLa
                           const int* grp_lo = nullptr,    // [n_groups+1] first slot per group (host-computed)
                           State* gscratch = nullptr,      // [B][n_groups] group states (warp-per-group kernel)
                           int* row_ctr = nullptr,         // [B] zeroed counters (warp-per-group kernel)
-                          const PushCtx* push = nullptr); // single group: also push the records (f2)
+                          const PushCtx* push = nullptr,  // single group: also push the records (f2)
+                          int grp_kernel = 0);            // grouped: 0 auto, 1 warp per (row, group), 3 block per row
 // Standalone sampler over materialised logits [B][ld] (bf16 or fp32): candidates per (V-block, row).
 cudaError_t launch_logits_sample(fs_dtype dtype, const void* logits, int64_t ld, const float* bias,
                                  const float* temperature, const uint32_t* mask, int64_t mask_words, int B, int V,

@@ -227,7 +227,7 @@ __global__ void gumbel_kernel(const uint32_t* r, float* g, int64_t n) {
 cudaError_t launch_reduce(const State* part, const int* part_group, const SlotLayout& lay, int B, int n_groups,
                           int32_t* idx_out, float* score_out, float* logZ_out, fs_summary* groups_out,
                           cudaStream_t stream, bool pdl, float* logprob_out, const int* grp_lo,
-                          State* gscratch, int* row_ctr, const PushCtx* push) {
+                          State* gscratch, int* row_ctr, const PushCtx* push, int grp_kernel) {
   cudaLaunchConfig_t cfg = {};
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -243,7 +243,11 @@ cudaError_t launch_reduce(const State* part, const int* part_group, const SlotLa
     return cudaLaunchKernelEx(&cfg, reduce_rows_kernel, part, part_group, lay.n_slots, B, idx_out, score_out,
                               logZ_out, groups_out, logprob_out, pc);
   }
-  if (grp_lo && gscratch && row_ctr && B <= 64) {   // measured: B=32 14.1 -> 10.3 us; B=256 19.4 -> 24.0
+  // warp per (row, group) up to B = 64, block per row above (ncu, Gemma-3-27B 65 groups: B=1 8.3 vs
+  // 10.2 us, B=32 10.8 vs 14.1, B=128 16.5 vs 14.2, B=256 23.5 vs 19.2; profiles/r02/stage2_ncu.csv)
+  const bool warp_ok = grp_lo && gscratch && row_ctr && B <= 256;
+  if (grp_kernel == 0) grp_kernel = (warp_ok && B <= 64) ? 1 : 3;
+  if (grp_kernel == 1 && warp_ok) {
     cfg.gridDim = dim3((n_groups + 7) / 8, B);
     cfg.blockDim = dim3(256);
     return cudaLaunchKernelEx(&cfg, reduce_groups_warp_kernel, part, B, n_groups, grp_lo, gscratch, row_ctr,

@@ -334,3 +334,25 @@ def test_contexts_per_stream_sample_concurrently():
     for res in outs:
         for (i, sc), (ri, rs) in zip(res, serial):
             assert np.array_equal(i.cpu().numpy(), ri) and np.array_equal(sc.cpu().numpy(), rs)
+
+
+@pytest.mark.parametrize("B", [1, 32, 300])
+def test_host_step_sampler_done_flag_serving_loop(B):
+    """HostStepSampler: the prepared fs_sample_staged call on a context of its own, completion by
+    spinning on the pinned done flag the finalizing CTA sets (option "done_flag") instead of a stream
+    sync.  A serving loop rewrites h_host between steps; every step's ids must equal the device path
+    on that step's h, and be complete when wait() returns."""
+    wl = synth.make_workload("llama3_8b", B, V=20011, D=256, seed_offset=B + 31)
+    W = wl.W.cuda()
+    h_host = torch.empty_like(wl.h).pin_memory()
+    s = fs.HostStepSampler(h_host, W, seed=wl.seed)
+    g = torch.Generator().manual_seed(B)
+    for step in range(6):
+        h_step = torch.randn(wl.h.shape, generator=g).to(torch.bfloat16)
+        h_host.copy_(h_step)
+        s(step)
+        got = s.wait().clone()
+        assert int(s.done[0]) == 1
+        ref = fs.sample(h_step.cuda(), W, seed=wl.seed, step=step)
+        torch.cuda.synchronize()
+        assert torch.equal(got, ref.cpu()), step

@@ -644,10 +644,10 @@ def run_single(args):
             "gpu_launches": (1 if one_kernel else 2) * args.steps * ((B + 255) // 256),
             "e2e": {"value": round(e2e_ms * 1e3, 2), "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": B * 4, "generic_call_us": round(e2e_generic_ms * 1e3, 2),
-                    "path": ("HostStepSampler (prepared fs_sample_staged call): the sampling kernel copies the "
-                             "pinned host h into device memory itself and stores the ids into pinned host memory; "
-                             "the host synchronises and reads the ids every step (generic_call_us: the same through "
-                             "sample_from_host)" if prepared else
+                    "path": ("HostStepSampler (prepared fs_sample_staged call on its own context): the sampling "
+                             "kernel copies the pinned host h into device memory itself, stores the ids into pinned "
+                             "host memory and then a pinned completion flag; the host spins on the flag and reads the "
+                             "ids every step (generic_call_us: sample_from_host + stream sync)" if prepared else
                              "sample_from_host: pinned inputs staged by fs_copy_async (PDL-chained copy kernel), "
                              "ids stored by the sampling kernel into pinned host memory; host sync + read every step")}}
     if not args.no_sweep:
@@ -658,6 +658,7 @@ def run_single(args):
             line["configs"]["paper_d4096"] = sweep(fs, "paper_d4096", pk, args, Bs=PAPER_B)
             line["tp_shards"] = tp_shards(fs, pk)
             line["tp_exchange_world1"] = tp_exchange_world1(fs)
+            line["tp_push_multiprocess_1gpu"] = tp_push_multiprocess()
     if not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(name, B, args.cpu_seconds)
     print(json.dumps(line), flush=True)
@@ -805,6 +806,19 @@ def tp_shards(fs, pk, name="llama3_70b", worlds=(2, 4, 8), Bs=(1, 32, 256)):
             del wl
     torch.cuda.empty_cache()
     return res
+
+
+def tp_push_multiprocess(world=2, steps=50, B=32):
+    """SURVEY f2 across processes: tools/tp_push_procs.py runs `world` ranks of the idx-only push step
+    on this one GPU (CUDA IPC windows); their kernels time-slice the GPU, so this checks the protocol
+    end to end (agreement, timeouts) rather than measuring an NVLink latency."""
+    try:
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "tp_push_procs.py"), str(world), str(steps),
+                            str(B)], capture_output=True, text=True, timeout=300)
+        lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+        return json.loads(lines[-1]) if lines else {"error": (r.stderr or r.stdout)[-300:]}
+    except Exception as e:  # pragma: no cover
+        return {"error": repr(e)[:200]}
 
 
 def tp_exchange_world1(fs, name="llama3_70b", n=8, Bs=(1, 32, 256)):

@@ -286,7 +286,7 @@ def time_graph(fn, n=50, reps=5):
     return statistics.median(ts)
 
 
-def timed_region(fn, steps, warmup, device_index=0, clock_window_s=0.12, barrier=None):
+def timed_region(fn, steps, warmup, device_index=0, clock_window_s=0.12, barrier=None, agree=None):
     """The contract's timed region: W warm-ups, then a pre-roll of the same step long enough that the
     clock sampler sees >= clock_window_s of this load, then sync (+ barrier), exactly K steps between
     CUDA events on the launching stream, sync (+ barrier).  Returns (ms per step, clocks summary)."""
@@ -296,6 +296,8 @@ def timed_region(fn, steps, warmup, device_index=0, clock_window_s=0.12, barrier
     torch.cuda.synchronize()
     est = time_loop(fn, 10, 0)
     n_pre = max(0, int(math.ceil(clock_window_s / max(1e-6, est * 1e-3))) - steps)
+    if agree is not None:            # N > 1: every rank must run the same number of (collective) steps
+        n_pre = agree(n_pre)
     with ClockSampler(device_index) as clk:
         for _ in range(n_pre):
             fn()
@@ -881,6 +883,11 @@ def tp_exchange_world1(fs, name="llama3_70b", n=8, Bs=(1, 32, 256)):
 
 
 # ----------------------------------------------------------------------------------------------
+def _trace(msg):
+    if os.environ.get("FS_BENCH_TRACE"):
+        print(f"[rank {os.environ.get('RANK', '0')}] {time.strftime('%H:%M:%S')} {msg}", file=sys.stderr, flush=True)
+
+
 def run_tp(args):
     import torch.distributed as dist
     import paper_2603_15854_b200 as fs
@@ -903,6 +910,7 @@ def run_tp(args):
     g.manual_seed(5678 + rank)
     W = (torch.randn(b - a, D, device=dev, generator=g) * synth.W_STD).to(torch.bfloat16)
     transport = "nccl" if backend == "nccl" else "torch"
+    _trace("init")
     if transport == "nccl":
         tp.NcclComm()                                     # the library's own communicator (fs_comm_init)
     local_s = fs.Summaries.empty(B, device=dev)
@@ -915,7 +923,13 @@ def run_tp(args):
         ctr[0] += 1
         return tp.sample_tp(h, W, a, V, seed=synth.SAMPLING_SEED, step=ctr[0], workspace=(local_s, gathered),
                             transport=transport, out=idx_buf)
-    ms_l, clocks = timed_region(step, args.steps, args.warmup, device_index=local, barrier=dist.barrier)
+
+    def agree(n):
+        t = torch.tensor([n], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return int(t.item())
+    _trace("timed")
+    ms_l, clocks = timed_region(step, args.steps, args.warmup, device_index=local, barrier=dist.barrier, agree=agree)
     ms = torch.tensor([ms_l], device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     idx = step()
@@ -935,34 +949,37 @@ def run_tp(args):
         idx_host.copy_(i, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         return int(idx_host[0])
+    _trace("e2e")
     e2e_l, _ = timed_region(e2e, args.steps, args.warmup, device_index=local, barrier=dist.barrier,
-                            clock_window_s=0.0)
+                            clock_window_s=0.0, agree=agree)
     e2e_ms = torch.tensor([e2e_l], device=dev)
     dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     # naive TP baseline: per-rank logits [B, V/n] bf16 -> all-gather -> sampler on the full row
+    _trace("naive")
     naive = {}
     try:
         lg_local = torch.empty(B, b - a, dtype=torch.bfloat16, device=dev)
         Vl = V // world
-        lg_all = torch.empty(world, B, Vl, dtype=torch.bfloat16, device=dev)
+        lg_all = torch.empty(world * B, Vl, dtype=torch.bfloat16, device=dev)   # concatenated (any backend)
 
         def naive_step():
             torch.matmul(h, W[:Vl].t(), out=lg_local[:, :Vl])
             dist.all_gather_into_tensor(lg_all, lg_local[:, :Vl].contiguous())
-            full = lg_all.permute(1, 0, 2).reshape(B, world * Vl).float()
+            full = lg_all.view(world, B, Vl).permute(1, 0, 2).reshape(B, world * Vl).float()
             try:
                 import flashinfer.sampling as fis
                 return fis.sampling_from_logits(full)
             except Exception:
                 return torch.multinomial(torch.softmax(full, -1), 1)
         n_ms, _ = timed_region(naive_step, args.steps, args.warmup, device_index=local, barrier=dist.barrier,
-                               clock_window_s=0.0)
+                               clock_window_s=0.0, agree=agree)
         n_t = torch.tensor([n_ms], device=dev)
         dist.all_reduce(n_t, op=dist.ReduceOp.MAX)
         naive = {"us_per_step": round(n_t.item() * 1e3, 2), "allgather_bytes_per_rank": 2 * B * Vl * (world - 1)}
     except Exception as e:  # pragma: no cover
         naive = {"error": repr(e)[:200]}
     # the same step with the library's peer-memory exchange instead of NCCL
+    _trace("push")
     push = {}
     ok = torch.ones(1, device=dev)
     try:
@@ -976,7 +993,7 @@ def run_tp(args):
             ctr[0] += 1
             return fs.sample_tp_push(h, W, a, V, seed=synth.SAMPLING_SEED, step=ctr[0])
         p_l, _ = timed_region(pstep, args.steps, args.warmup, device_index=local, barrier=dist.barrier,
-                              clock_window_s=0.0)
+                              clock_window_s=0.0, agree=agree)
         p_ms = torch.tensor([p_l], device=dev)
         dist.all_reduce(p_ms, op=dist.ReduceOp.MAX)
         pidx = pstep()
@@ -986,6 +1003,7 @@ def run_tp(args):
         dist.all_reduce(same, op=dist.ReduceOp.MIN)
         push = {"us_per_step": round(p_ms.item() * 1e3, 2), "idx_equal_nccl_path": bool(same.item() == 1),
                 "timeouts": fs.query("comm_timeouts")}
+    _trace("report")
     if rank == 0:
         pk = peaks()
         us = ms.item() * 1e3

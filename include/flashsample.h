@@ -279,10 +279,12 @@ fs_status fs_combine_summaries(const fs_summary* gathered, int n, int B,
  * fs_comm_window_open: map the peers' windows from the gathered handles [world] (entry `rank`
  *   is ignored).  Peers may be other GPUs (peer access over NVLink) or the same GPU.
  * fs_sample_tp_push: fs_sample_shard + push + wait + fs_combine_summaries in stream order;
- *   every rank gets the identical idx_out (score_out, logZ_out optional).  For B <= 256 the push is
- *   fused into the shard sampler's last reduction step (the finalizing stage-1 CTA for B <= 16,
- *   else the stage-2 row reduce): it stores the records into every peer window and releases the
- *   flags itself, and one PDL-chained single-block kernel waits for the n flags and combines.
+ *   every rank gets the identical idx_out (score_out, logZ_out optional).  Without logZ_out (B <= 256,
+ *   bf16 tcgen05 path): ONE kernel per rank -- the shard sampler's finalizing CTA stores the records
+ *   into every peer window, releases its flags, waits for the n ranks' records, runs the outer
+ *   selection and acknowledges the epoch.  With logZ_out (B <= 256) the push is fused into the
+ *   shard sampler's log-mass reduction step (the finalizing stage-1 CTA for B <= 16, else the
+ *   stage-2 row reduce) and one PDL-chained single-block kernel waits for the n flags and combines.
  *   Larger B push from a separate kernel.  All ranks must call it the same number of times (the
  *   step epoch is a per-context counter).  A peer that does not arrive within ~10 s makes the wait
  *   give up: idx_out = -1 and fs_ctx_query("comm_timeouts") counts it.

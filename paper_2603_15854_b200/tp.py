@@ -16,8 +16,10 @@ Three transports, all with the arithmetic in the library kernels:
   * "torch" (default on gloo): fs_sample_shard, torch.distributed all-gather, fs_combine_summaries.
   * push    (PushExchange + sample_tp_push_step): the library's peer-memory exchange
             -- the shard kernel stores its records straight into every peer's window (CUDA IPC;
-            NVLink stores between GPUs) and one small kernel waits for the n records and combines.
-            The group is used once, to all-gather the 64-byte window handles.
+            NVLink stores between GPUs).  Idx only: the same kernel's finalizing CTA then waits for
+            the n records and combines (one kernel per rank and step); with logZ one small
+            PDL-chained kernel waits and combines.  The group is used once, to all-gather the 64-byte
+            window handles.
 """
 from __future__ import annotations
 

@@ -401,6 +401,7 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
       p.dbg_no_mma = ctx->dbg_no_mma;
       p.dbg_no_epi = ctx->dbg_no_epi;
       p.dbg_times = ctx->dbg_times;
+      p.need_lt = a.logprob_out != nullptr;
       p.w_policy = ctx->w_policy;
       p.epi_sleep = ctx->epi_sleep;
       p.spin_wait = ctx->spin_wait;

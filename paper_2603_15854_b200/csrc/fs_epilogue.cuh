@@ -66,6 +66,7 @@ struct EpiArgs {
   int row_offset;           // global batch index of column 0 (RNG counter)
   uint32_t k0, k1, c2, c3;  // Philox key and counter words 2, 3
   int dbg_skip;             // debug: drain TMEM without computing (bounds the MMA+TMA-only time)
+  int need_lt;              // log-mass epilogue: also carry the winner's l~ (only log-prob outputs read it)
 };
 
 // One-kernel finalize (StageOneParams::fin_best).  The candidate order of state_merge (larger key,
@@ -345,11 +346,13 @@ __device__ __forceinline__ void epi_tile_tc(uint32_t taddr, const RowArgs& ra, c
           if (o <= bit) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
         constexpr int kShift = (NC == 16) ? 1 : 2;          // column of lane L = L >> kShift
         const float Sw = __shfl_sync(0xFFFFFFFFu, v, (jo & (NC - 1)) << kShift);
-        float ltw = 0.0f;                                    // l~ of each column's winner
+        float ltw = 0.0f;                                    // l~ of each column's winner (log-prob only)
+        if (ea.need_lt) {
 #pragma unroll
-        for (int jj = 0; jj < NC; ++jj) {
-          const float x = __shfl_sync(0xFFFFFFFFu, lt[jj], kmax[jj] > kKeyNone ? __ffs(ball[jj]) - 1 : 0);
-          ltw = (jo == jj) ? x : ltw;
+          for (int jj = 0; jj < NC; ++jj) {
+            const float x = __shfl_sync(0xFFFFFFFFu, lt[jj], kmax[jj] > kKeyNone ? __ffs(ball[jj]) - 1 : 0);
+            ltw = (jo == jj) ? x : ltw;
+          }
         }
         if (mine) absorb<true>(own, km, wi, Sw, ltw);
       } else {

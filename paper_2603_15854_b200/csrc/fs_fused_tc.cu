@@ -292,6 +292,7 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
     ea.c2 = ctr_step_lo(p.step);
     ea.c3 = ctr_step_hi(p.step, 0u);
     ea.dbg_skip = p.dbg_no_epi;
+    ea.need_lt = p.need_lt;
     State st[8];
 #pragma unroll
     for (int c = 0; c < 8; ++c) st[c] = state_empty();

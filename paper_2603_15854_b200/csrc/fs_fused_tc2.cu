@@ -219,6 +219,7 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
     ea.c2 = ctr_step_lo(p.step);
     ea.c3 = ctr_step_hi(p.step, 0u);
     ea.dbg_skip = p.dbg_no_epi;
+    ea.need_lt = p.need_lt;
     const uint32_t tempty_leader = sm100::mapa(sm100::smem_u32(&tempty[set]), 0);
     State st[4];
 #pragma unroll

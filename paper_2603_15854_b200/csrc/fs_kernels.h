@@ -87,6 +87,7 @@ struct StageOneParams {
   float* logZ_out;                // [B] or nullptr
   fs_summary* groups_out;         // [B] (the single group's summary, e.g. a TP shard's) or nullptr
   float* logprob_out;             // [B] or nullptr
+  int need_lt;                    // some output of the call reads the winner's l~ (log-prob)
   unsigned long long* dbg_times;  // debug: [grid][8] globaltimer ns (start, dependency wait done, last load
                                   // issued, last tile drained), %smid, CTA done, 0, 0; or nullptr
   const void* h_host;             // in-kernel staging (fs_sample_staged): pinned host h copied into h by

@@ -101,7 +101,7 @@ struct fs_ctx {
   struct MapEnt { MapKey k; CUtensorMap m; };
   std::vector<MapEnt> map_cache;
   // per-(CTA, segment) W descriptors in device memory (fs_fused_tc.cu), cached per layout
-  struct SegKey { const void* W; int64_t D; int V, G, unit, gs, promo; };
+  struct SegKey { const void* W; int64_t D; int V, G, unit, gs, promo, pair, gran; };
   struct SegEnt { SegKey k; CUtensorMap* dev; int max_seg; };
   std::vector<SegEnt> seg_cache;
   // grouped stage 2: first candidate slot of every group ([n_groups + 1], device), per slot layout
@@ -227,11 +227,13 @@ void host_cta_rows(int cta, int G, int V, int unit, int& r0, int& r1) {
   r1 = (int)(e < (int64_t)V ? e : (int64_t)V);
 }
 
+// Box rows per segment = the kernel's tile rows (fs::seg_tile_rows): the 1-CTA kernel's tiles, or
+// this CTA's half of the CTA-pair tile (pair = 1).
 fs_status segment_maps(fs_ctx* ctx, const void* W, int64_t D, int V, int G, int unit, int gs,
-                       const CUtensorMap** out, int* max_seg_out) {
+                       const CUtensorMap** out, int* max_seg_out, int pair = 0, int gran = 8) {
   for (const auto& e : ctx->seg_cache)
     if (e.k.W == W && e.k.D == D && e.k.V == V && e.k.G == G && e.k.unit == unit && e.k.gs == gs &&
-        e.k.promo == ctx->l2promo) {
+        e.k.promo == ctx->l2promo && e.k.pair == pair && e.k.gran == gran) {
       *out = e.dev;
       *max_seg_out = e.max_seg;
       return FS_OK;
@@ -252,7 +254,8 @@ fs_status segment_maps(fs_ctx* ctx, const void* W, int64_t D, int V, int G, int 
       const int b = std::min(r1, (a / gs + 1) * gs);
       const cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)(b - a)};
       const cuuint64_t strides[1] = {(cuuint64_t)D * 2};
-      const cuuint32_t box[2] = {64u, 128u};
+      const int T = pair ? fs::seg_tile_rows(b - a, 256, 16) / 2 : fs::seg_tile_rows(b - a, 128, gran);
+      const cuuint32_t box[2] = {64u, (cuuint32_t)T};
       const cuuint32_t estr[2] = {1u, 1u};
       CUresult r = ctx->encode(&maps[(size_t)c * max_seg + s], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                                const_cast<char*>(static_cast<const char*>(W)) + (size_t)a * D * 2, dims, strides, box,
@@ -271,7 +274,7 @@ fs_status segment_maps(fs_ctx* ctx, const void* W, int64_t D, int V, int G, int 
   if (e != cudaSuccess) return fail(FS_ERR_OOM, std::string("descriptor cudaMalloc failed: ") + cudaGetErrorString(e) + kAllocHint);
   e = cudaMemcpy(dev, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return cuda_fail(e, "descriptor upload");
-  ctx->seg_cache.push_back(fs_ctx::SegEnt{fs_ctx::SegKey{W, D, V, G, unit, gs, ctx->l2promo}, dev, max_seg});
+  ctx->seg_cache.push_back(fs_ctx::SegEnt{fs_ctx::SegKey{W, D, V, G, unit, gs, ctx->l2promo, pair, gran}, dev, max_seg});
   *out = dev;
   *max_seg_out = max_seg;
   return FS_OK;
@@ -342,7 +345,8 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
   int max_seg = 1, n_slots;
   const CUtensorMap* wmaps = nullptr;
   if (tc) {
-    fs_status st0 = segment_maps(ctx, a.W, a.D, a.V, units, unit, std::min(a.group_size, a.V), &wmaps, &max_seg);
+    fs_status st0 = segment_maps(ctx, a.W, a.D, a.V, units, unit, std::min(a.group_size, a.V), &wmaps, &max_seg,
+                                 pair ? 1 : 0);
     if (st0 != FS_OK) return st0;
     n_slots = (a.group_size >= a.V) ? G : G * max_seg * fs::tc_slots_per_segment();
   } else {
@@ -554,7 +558,7 @@ fs_status run_topk_path(fs_ctx* ctx, const PathArgs& a, int k, float top_p, cuda
   const CUtensorMap* wmaps = nullptr;
   int max_seg = 1;
   if (tc) {
-    fs_status st0 = segment_maps(ctx, a.W, a.D, a.V, G, unit, a.V, &wmaps, &max_seg);
+    fs_status st0 = segment_maps(ctx, a.W, a.D, a.V, G, unit, a.V, &wmaps, &max_seg, 0, 16);   // top-k modes
     if (st0 != FS_OK) return st0;
   }
   // workspace: candidates [Bc][G*k] (lists) or logits [Bc][V] fp32 + chunk candidates

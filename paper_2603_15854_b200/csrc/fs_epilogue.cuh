@@ -610,8 +610,5 @@ __device__ __forceinline__ void cta_rows(int cta, int G, int V, int unit, int& r
   const int64_t e = unit * ((int64_t)(cta + 1) * U / G);
   r1 = (int)(e < (int64_t)V ? e : (int64_t)V);
 }
-// Tiles are the intersections of the CTA's rows with 128-aligned blocks, so a tile never
-// straddles a group boundary (group sizes are multiples of 128).
-__device__ __forceinline__ int tile_end(int t0, int r1) { return min(r1, (t0 & ~127) + 128); }
 
 }  // namespace fs

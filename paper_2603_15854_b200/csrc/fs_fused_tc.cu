@@ -119,13 +119,16 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
   cta_rows(blockIdx.x, gridDim.x, p.V, p.unit_rows, r0, r1);
   const int num_kb = (p.D + kBlockK - 1) / kBlockK;
   const int gs = p.group_size;
+  // tile rows a multiple of 8 (the swizzle atom); 16 in the top-k modes, whose span maxima are
+  // indexed by 16-row unit (fs_topk.cu)
+  constexpr int kTileGran = MODE == 0 ? 8 : 16;
 
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------ TMA producer ------------------------------------
       const uint64_t pol_w = p.w_policy ? sm100::policy_evict_first() : sm100::policy_evict_normal();
       const uint64_t pol_h = sm100::policy_evict_last();
-      const uint32_t stage_tx = (uint32_t)(kWStageBytes + h_stage_bytes);   // full boxes, OOB counted
+      // full boxes (OOB-clipped rows still counted): T_seg rows of W + the h tile per K slice
       // PDL: the first S stages' W loads are issued before the dependency wait; their h loads
       // (the stage barrier still expects those bytes) are deferred until it returns.
       auto load_h = [&](int stg, int kb0, int nk) {
@@ -150,7 +153,9 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
       for (int a = r0; a < r1; ++seg) {
         const int b = seg_end(a, r1, gs);
         const CUtensorMap* wm = &wmaps[seg];
-        for (int t0 = a; t0 < b; t0 += kBlockM) {
+        const int T = seg_tile_rows(b - a, kBlockM, kTileGran);
+        const uint32_t stage_tx = (uint32_t)(T * kBlockK * 2 + h_stage_bytes);
+        for (int t0 = a; t0 < b; t0 += T) {
           for (int kb0 = 0; kb0 < num_kb; kb0 += KBPS) {
             const int nk = min(KBPS, num_kb - kb0);
             sm100::mbar_wait(&empty[stage], phase ^ 1);
@@ -186,7 +191,8 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
       int tile_i = 0;
       for (int a = r0; a < r1;) {
         const int b = seg_end(a, r1, gs);
-        for (int t0 = a; t0 < b; t0 += kBlockM, ++tile_i) {
+        const int T = seg_tile_rows(b - a, kBlockM, kTileGran);
+        for (int t0 = a; t0 < b; t0 += T, ++tile_i) {
           const int buf = tile_i & 1;
           const uint32_t use = (uint32_t)(tile_i >> 1);
           sm100::mbar_wait(&tempty[buf], (use & 1) ^ 1);
@@ -227,12 +233,13 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
     int tile_i = 0;
     for (int a = r0; a < r1;) {
       const int b = seg_end(a, r1, gs);
-      for (int t0 = a; t0 < b; t0 += kBlockM, ++tile_i) {
+      const int T = seg_tile_rows(b - a, kBlockM, kTileGran);
+      for (int t0 = a; t0 < b; t0 += T, ++tile_i) {
         const int buf = tile_i & 1;
         const uint32_t use = (uint32_t)(tile_i >> 1);
         sm100::mbar_wait(&tfull[buf], use & 1);
         sm100::tc_fence_after();
-        const int t1 = min(b, t0 + kBlockM);
+        const int t1 = min(b, t0 + T);
         const int row = t0 + 32 * q + lane;
         RowArgs ra;
         ra.valid = row < t1;
@@ -261,14 +268,15 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
     int tile_i = 0;
     for (int a = r0; a < r1;) {
       const int b = seg_end(a, r1, gs);
-      for (int t0 = a; t0 < b; t0 += kBlockM, ++tile_i) {
+      const int T = seg_tile_rows(b - a, kBlockM, kTileGran);
+      for (int t0 = a; t0 < b; t0 += T, ++tile_i) {
         if ((tile_i & 1) != set) continue;
         const uint32_t use = (uint32_t)(tile_i >> 1);
         sm100::mbar_wait(&tfull[set], use & 1);
         sm100::tc_fence_after();
         const int row = t0 + 32 * q + lane;
         const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(set * BN);
-        const int span0 = t0 + 32 * q, t1 = min(b, t0 + kBlockM);
+        const int span0 = t0 + 32 * q, t1 = min(b, t0 + T);
         epi_tile_store(taddr, row < t1, row, p.B, p.mat_out, p.mat_ld, p.topk_gmax, p.topk_gld, span0 >> 4,
                        max(0, min(32, t1 - span0)), lane);
         release_tmem(&tempty[set], 0, lane);
@@ -300,9 +308,10 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
     int tile_i = 0, seg = 0;
     for (int a = r0; a < r1; ++seg) {
       const int b = seg_end(a, r1, gs);
-      for (int t0 = a; t0 < b; t0 += kBlockM, ++tile_i) {
+      const int T = seg_tile_rows(b - a, kBlockM, kTileGran);
+      for (int t0 = a; t0 < b; t0 += T, ++tile_i) {
         if ((tile_i & 1) != set) continue;
-        const int t1 = min(b, t0 + kBlockM);
+        const int t1 = min(b, t0 + T);
         const uint32_t use = (uint32_t)(tile_i >> 1);
         if (p.epi_sleep) sm100::mbar_wait_sleep(&tfull[set], use & 1, (uint32_t)p.epi_sleep);
         else if (p.spin_wait) sm100::mbar_wait_spin(&tfull[set], use & 1);   // A/B only

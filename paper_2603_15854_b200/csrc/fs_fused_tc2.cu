@@ -113,7 +113,7 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
       // -------------------------- TMA producer (both CTAs) ------------------------------
       const uint64_t pol_w = p.w_policy ? sm100::policy_evict_first() : sm100::policy_evict_normal();
       const uint64_t pol_h = sm100::policy_evict_last();
-      const uint32_t pair_tx = 2u * (uint32_t)(kWBytes + h_bytes);
+      // per K slice: both CTAs' Th rows of W (full boxes, OOB-clipped rows counted) + both h halves
       // PDL: W loads of the first S stages before the dependency wait, their h loads after it
       auto load_h = [&](int stg, int kb0, int nk) {
         for (int j = 0; j < nk; ++j)
@@ -137,7 +137,9 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
       for (int a = r0; a < r1; ++seg) {
         const int b = seg_end2(a, r1, gs);
         const CUtensorMap* wm = &wmaps[seg];
-        for (int t0 = a; t0 < b; t0 += 256) {
+        const int T2 = seg_tile_rows(b - a, 256, 16), Th = T2 / 2;   // pair tile, this CTA's half
+        const uint32_t pair_tx = 2u * (uint32_t)(Th * kBlockK * 2 + h_bytes);
+        for (int t0 = a; t0 < b; t0 += T2) {
           for (int kb0 = 0; kb0 < num_kb; kb0 += KBPS) {
             const int nk = min(KBPS, num_kb - kb0);
             sm100::mbar_wait(&empty[stage], phase ^ 1);
@@ -149,7 +151,7 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
             if (rank == 0) sm100::mbar_arrive_expect_tx(&full[stage], pair_tx * nk);
             for (int j = 0; j < nk; ++j)
               sm100::tma_load_2d_pair(w_ring + ((size_t)stage * KBPS + j) * kWBytes, wm, &full[stage],
-                                      (kb0 + j) * kBlockK, t0 - a + 128 * (int)rank, pol_w);
+                                      (kb0 + j) * kBlockK, t0 - a + Th * (int)rank, pol_w);
             if (waited) {
               load_h(stage, kb0, nk);
             } else {
@@ -173,7 +175,8 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
       int tile_i = 0;
       for (int a = r0; a < r1;) {
         const int b = seg_end2(a, r1, gs);
-        for (int t0 = a; t0 < b; t0 += 256, ++tile_i) {
+        const int T2 = seg_tile_rows(b - a, 256, 16);
+        for (int t0 = a; t0 < b; t0 += T2, ++tile_i) {
           const int buf = tile_i & 1;
           const uint32_t use = (uint32_t)(tile_i >> 1);
           sm100::mbar_wait(&tempty[buf], (use & 1) ^ 1);
@@ -228,16 +231,17 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
     int tile_i = 0, seg = 0;
     for (int a = r0; a < r1; ++seg) {
       const int b = seg_end2(a, r1, gs);
-      for (int t0 = a; t0 < b; t0 += 256, ++tile_i) {
+      const int T2 = seg_tile_rows(b - a, 256, 16), Th = T2 / 2;
+      for (int t0 = a; t0 < b; t0 += T2, ++tile_i) {
         if ((tile_i & 1) != set) continue;
         const uint32_t use = (uint32_t)(tile_i >> 1);
         if (p.spin_wait) sm100::mbar_wait_spin(&tfull[set], use & 1);   // A/B only
         else sm100::mbar_wait(&tfull[set], use & 1);
         sm100::tc_fence_after();
-        const int base = t0 + 128 * (int)rank;
+        const int base = t0 + Th * (int)rank;
         const int row = base + 32 * q + lane;
         RowArgs ra;
-        ra.valid = row < b;
+        ra.valid = 32 * q + lane < Th && row < b;
         ra.v_global = (int32_t)(p.vocab_offset + row);
         ra.v_lo = (uint32_t)ra.v_global;
         ra.warp_v0 = (int32_t)(p.vocab_offset + base + 32 * q);

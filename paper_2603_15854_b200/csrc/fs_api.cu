@@ -334,11 +334,16 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
     return run_path(ctx, b, stream);
   }
   const size_t esz = a.dtype == FS_BF16 ? 2 : 4;
-  const int unit = ctx->unit_rows > 0 ? ctx->unit_rows : 16;
-  const int U = (a.V + unit - 1) / unit;
   const int BN_first = fs::tc_block_n(std::min(a.B, 256));
   const bool pair = tc && (ctx->pair == 1 || (ctx->pair < 0 && BN_first >= ctx->pair_min_bn)) &&
                     (ctx->max_ctas > 0 ? ctx->max_ctas : ctx->num_sms) >= 2;
+  // CTA range granularity: 16 rows, except grouped calls on the tensor-core kernels, which cut
+  // ranges in whole tiles (128 rows, 256 per CTA pair): group sizes are multiples of 128, so every
+  // segment is then whole tiles -- with 16-row ranges almost every CTA straddles a group boundary
+  // and pays one extra, partial tile pass (Gemma-3-27B: 15 instead of 14 passes, §11 entry 28)
+  const int unit = ctx->unit_rows > 0 ? ctx->unit_rows
+                                      : (tc && a.group_size < a.V && a.group_size % 256 == 0) ? (pair ? 256 : 128) : 16;
+  const int U = (a.V + unit - 1) / unit;
   // persistent grid: #SMs CTAs (or #SMs/2 pairs), never more work units than rows allow
   const int units = std::min(std::max(1, (ctx->max_ctas > 0 ? ctx->max_ctas : ctx->num_sms) / (pair ? 2 : 1)), U);
   const int G = units * (pair ? 2 : 1);

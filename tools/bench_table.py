@@ -3,7 +3,11 @@
 import json
 import sys
 
-d = json.loads([ln for ln in open(sys.argv[1]).read().strip().splitlines() if ln.startswith("{")][-1])
+_txt = open(sys.argv[1]).read().strip()
+try:
+    d = json.loads(_txt)                      # a pretty-printed bench.json
+except json.JSONDecodeError:                  # a bench log: the last JSON line
+    d = json.loads([ln for ln in _txt.splitlines() if ln.startswith("{")][-1])
 print("| config | B | per call | loop | pipelined | bound, frac (of floor) | cuBLAS GEMM only | Multinomial eager / compiled | FI2 | FI1 | × best unfused | × GEMM only |")
 print("|---|---|---|---|---|---|---|---|---|---|---|---|")
 sweeps = [("llama3_8b", d.get("sweep", {}))] + list(d.get("configs", {}).items())

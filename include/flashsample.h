@@ -110,6 +110,11 @@ void fs_ctx_destroy(fs_ctx* ctx);
  *       system-scope release after every output of the call is written, so a serving loop can spin
  *       on host memory (reset it to 0 before the call) instead of synchronising the stream.  Per
  *       context: give the waiting loop a context of its own.  0 = off.
+ *   "whole_tiles" (default 1): single-group calls on the tensor-core kernels cut the vocabulary into
+ *       whole tiles (128 rows, 256 per CTA pair) and run on the fewest CTAs (pairs) that still need
+ *       only P = ceil(tiles / #SMs) tile passes, each CTA taking P or P-1 full tiles (V = 152,064:
+ *       132 CTAs x 9 tiles instead of 148 CTAs with partial tiles).  Ignored when "max_ctas" or
+ *       "unit_rows" is set.  0 = 16-row CTA ranges on every SM.  Same results bit for bit.
  *   Tuning / testing: "force_simt" (1 = CUDA-core kernel), "max_ctas" (cap the persistent grid,
  *   0 = number of SMs), "pdl" (stage 1 -> stage 2 programmatic launch, default 1), "pair" (CTA-pair
  *   kernel: -1 auto, 0 off, 1 on), "stages", "kbps", "unit_rows", "l2promo", "w_policy",

@@ -73,6 +73,8 @@ struct fs_ctx {
   int grp_ranges = 1;              // grouped stage 2: host-computed group slot ranges (0 = device binary search)              // raw-logit route: span maxima + gather (1) or full chunk selection (0)
   int* topk_rowcnt = nullptr;      // [256] per-row candidate counters of the list route (kept at 0 between calls)
   int fuse_reduce = 1;             // single-group sampling without log-mass: last CTA finalizes (no stage 2)
+  int whole_tiles = 1;             // single-group tensor-core calls: whole-tile CTA ranges on the fewest CTAs
+                                   // that keep the pass count (0 = 16-row ranges; DESIGN.md §11 entry 29)
   int pdl_w = 0;                   // stage 1 launched with PDL, W streamed before the dependency wait
                                    // (1: for batch chunks <= pdl_w_max_b rows, 2: always)
   int pdl_w_max_b = 128;
@@ -341,11 +343,21 @@ fs_status run_path(fs_ctx* ctx, const PathArgs& a, cudaStream_t stream) {
   // ranges in whole tiles (128 rows, 256 per CTA pair): group sizes are multiples of 128, so every
   // segment is then whole tiles -- with 16-row ranges almost every CTA straddles a group boundary
   // and pays one extra, partial tile pass (Gemma-3-27B: 15 instead of 14 passes, §11 entry 28)
-  const int unit = ctx->unit_rows > 0 ? ctx->unit_rows
-                                      : (tc && a.group_size < a.V && a.group_size % 256 == 0) ? (pair ? 256 : 128) : 16;
+  int unit = ctx->unit_rows > 0 ? ctx->unit_rows
+                                : (tc && a.group_size < a.V && a.group_size % 256 == 0) ? (pair ? 256 : 128) : 16;
   const int U = (a.V + unit - 1) / unit;
   // persistent grid: #SMs CTAs (or #SMs/2 pairs), never more work units than rows allow
-  const int units = std::min(std::max(1, (ctx->max_ctas > 0 ? ctx->max_ctas : ctx->num_sms) / (pair ? 2 : 1)), U);
+  int units = std::min(std::max(1, (ctx->max_ctas > 0 ? ctx->max_ctas : ctx->num_sms) / (pair ? 2 : 1)), U);
+  if (ctx->whole_tiles && tc && ctx->max_ctas <= 0 && ctx->unit_rows <= 0 && a.group_size >= a.V) {
+    // whole-tile ranges: P = ceil(tiles / units) tile passes are unavoidable; the fewest CTAs (pairs)
+    // that still need only P passes get P or P-1 full tiles each (V = 152,064: 132 CTAs x 9 tiles
+    // instead of 148 CTAs, some with 9 passes of 116 rows)
+    const int tile = pair ? 256 : 128;
+    const int tiles = (a.V + tile - 1) / tile;
+    const int P = (tiles + units - 1) / units;
+    units = (tiles + P - 1) / P;
+    unit = tile;
+  }
   const int G = units * (pair ? 2 : 1);
   int max_seg = 1, n_slots;
   const CUtensorMap* wmaps = nullptr;
@@ -761,6 +773,7 @@ fs_status fs_ctx_set_option(fs_ctx* ctx, const char* name, int64_t value) {
   else if (!strcmp(name, "epi_sleep")) ctx->epi_sleep = (int)value;
   else if (!strcmp(name, "pair")) ctx->pair = (int)value;
   else if (!strcmp(name, "fuse_reduce")) ctx->fuse_reduce = (int)value;
+  else if (!strcmp(name, "whole_tiles")) ctx->whole_tiles = (int)value;
   else if (!strcmp(name, "topk_spans")) ctx->topk_spans = (int)value;
   else if (!strcmp(name, "grp_ranges")) ctx->grp_ranges = (int)value;
   else if (!strcmp(name, "pdl_w")) ctx->pdl_w = (int)value;

@@ -33,7 +33,8 @@ def _run(wl, step, **kw):
 def _reset_options():
     yield
     if torch.cuda.is_available():
-        for k, v in (("force_simt", 0), ("max_ctas", 0), ("pdl", 1), ("stages", 0), ("pair", -1), ("kbps", 0), ("fuse_reduce", 1), ("pdl_w", 0)):
+        for k, v in (("force_simt", 0), ("max_ctas", 0), ("pdl", 1), ("stages", 0), ("pair", -1), ("kbps", 0), ("fuse_reduce", 1), ("pdl_w", 0),
+                     ("whole_tiles", 1)):
             fs.set_option(k, v)
 
 
@@ -116,6 +117,23 @@ def test_grid_invariance_bit_exact(max_ctas):
     idx, score = _run(wl, 9)
     assert np.array_equal(idx, ref_idx)
     assert np.array_equal(score.view(np.uint32), ref_score.view(np.uint32))
+
+
+@pytest.mark.parametrize("config,B,V", [("llama3_8b", 1, 152064), ("qwen25_7b", 32, 152064), ("llama3_8b", 256, 151936),
+                                        ("qwen25_7b", 8, 16032), ("llama3_8b", 64, 1000), ("qwen25_7b", 200, 40000)])
+def test_whole_tile_grid_bit_exact(config, B, V):
+    # whole_tiles (default): fewest CTAs (pairs) with whole 128/256-row tiles; 0: 16-row ranges on
+    # every SM.  The partition never changes a logit's accumulation -> identical results.
+    wl = synth.make_workload(config, B, V=V, D=64, seed_offset=77 + B)
+    fs.set_option("whole_tiles", 0)
+    ref = _run(wl, 3)
+    fs.set_option("whole_tiles", 1)
+    got = _run(wl, 3)
+    assert np.array_equal(got[0], ref[0])
+    assert np.array_equal(got[1].view(np.uint32), ref[1].view(np.uint32))
+    if V <= 40000:
+        _, flat = oracle_flat(wl, 3)
+        check_flat(*got, flat)
 
 
 def test_stage_ring_depth_and_pdl_invariance():

@@ -3,6 +3,7 @@ and the SM clock / power sampled during each loop.  Every combination is measure
 interleaved order (A B A B ...) so that clock drift under the power cap hits all of them alike.
 
     python tools/sweep_opts.py llama3_8b 128,256 '{"dbg_no_epi": [0, 1]}'
+    VDIV=8 python tools/sweep_opts.py llama3_70b 1,32 '{"whole_tiles": [0, 1]}'   # V/8 rows (a TP shard's compute)
 """
 import itertools
 import json
@@ -25,7 +26,8 @@ dev = torch.device("cuda", 0)
 pk = bench.peaks()
 fs.set_option("pdl_w", 0)
 for B in Bs:
-    wl = bench.make_device_workload(name, B, dev)
+    vdiv = int(os.environ.get("VDIV", "1"))
+    wl = bench.make_device_workload(name, B, dev, V=bench.synth.CONFIGS[name]["V"] // vdiv if vdiv > 1 else None)
     out = torch.empty(B, dtype=torch.int32, device=dev)
     keys = list(opts)
     fn0 = bench.fused_step_fn(fs, wl, [0], out)

@@ -4,6 +4,7 @@ interleaved order (A B A B ...) so that clock drift under the power cap hits all
 
     python tools/sweep_opts.py llama3_8b 128,256 '{"dbg_no_epi": [0, 1]}'
     VDIV=8 python tools/sweep_opts.py llama3_70b 1,32 '{"whole_tiles": [0, 1]}'   # V/8 rows (a TP shard's compute)
+    python tools/sweep_opts.py llama3_8b 256 '[{"h_lead": -1}, {"h_lead": 4, "kbps": 2, "h_stages": 3}]'   # explicit combos
 """
 import itertools
 import json
@@ -29,14 +30,18 @@ for B in Bs:
     vdiv = int(os.environ.get("VDIV", "1"))
     wl = bench.make_device_workload(name, B, dev, V=bench.synth.CONFIGS[name]["V"] // vdiv if vdiv > 1 else None)
     out = torch.empty(B, dtype=torch.int32, device=dev)
-    keys = list(opts)
+    if isinstance(opts, list):                      # explicit combinations: [{"opt": v, ...}, ...]
+        keys = sorted({k for d in opts for k in d})
+        combos = [tuple(d.get(k, 0) for k in keys) for d in opts]
+    else:
+        keys = list(opts)
+        combos = list(itertools.product(*[opts[k] for k in keys]))
     fn0 = bench.fused_step_fn(fs, wl, [0], out)
     t_end = time.time() + 1.0
     while time.time() < t_end:                     # pre-heat: let clocks settle under load
         for _ in range(50):
             fn0()
         torch.cuda.synchronize()
-    combos = list(itertools.product(*[opts[k] for k in keys]))
     res = {c: [] for c in combos}
     for rep in range(REPS):
         for combo in combos:

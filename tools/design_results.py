@@ -51,8 +51,9 @@ and B = 1–8 rows where both are at the copy peak. The north star's bar, beatin
 holds on every row (× best unfused ≥ 1.16).
 
 ncu (`profiles/r02/ncu_full_summary.json` / `.txt`, `--set full`, one call per config and B): DRAM
-bytes per stage-1 launch 1.006–1.009 × the algorithmic bytes on every config (W once; no logits
-written: DRAM writes 3–12 MB); L2→SM 1.16 × W at B ≤ 32, 2.07 × W at B = 256 (h re-read per tile);
+bytes per stage-1 launch 1.001–1.006 × the algorithmic bytes on every full-vocabulary config, 1.006–1.019 × on the
+70B shards (W once; no logits
+written: DRAM writes 3–12 MB); L2→SM 1.12 × W at B ≤ 32, 2.0 × W at B = 256 (h re-read per tile);
 tensor pipe 5–10% active at B ≤ 32, 60–77% at B = 256 (1.34–1.51 GHz under the cap). Launch list of
 the headline bench command: the fused kernel is 96% of the process's GPU time, one launch per step
 (`profiles/r02/launches_b32_summary.json`).

@@ -22,6 +22,10 @@ for pair in (0, 1):
     parts = [fs.sample_shard(h, W[a:b].contiguous(), a, 3000, seed=1, step=2).raw for a, b in ((0, 1500), (1500, 3000))]
     fs.combine_summaries(torch.stack(parts))
 fs.set_option("pair", -1)
+for wt in (0, 1):                                         # 16-row CTA ranges / whole tiles on the fewest CTAs
+    fs.set_option("whole_tiles", wt)
+    fs.sample(h, W, bias=bias, temperature=tau, mask=mask, seed=1, step=4, return_score=True)
+    fs.sample(h[:8].contiguous(), W, seed=1, step=4)
 # one-kernel paths added later: logZ finalize in the last CTA (B <= 16), grouped warp-per-group stage 2,
 # in-kernel host staging, logits-sampler finalize, fused top-k span gather
 h8, tau8, mask8 = h[:8].contiguous(), tau[:8].contiguous(), mask[:8].contiguous()

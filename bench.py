@@ -539,6 +539,18 @@ def roofline(name, B, D, V, t_kernel_ms, pk, transforms, kname=None, traffic_key
             "frac_of_nominal_8TBps": round(ach / 8000.0, 4), **common}
 
 
+def read_peak(fs, dev, nbytes=1 << 30, iters=20):
+    """Read-only HBM peak: our bulk-TMA read ring (fs_read_probe) over a 1 GiB random
+    buffer (8.5x L2), CUDA events around `iters` back-to-back launches after warm-up.  The copy peak
+    of MEASURED_PEAKS.json stays the roofline denominator; this is the read-only ceiling beside it."""
+    buf = torch.empty(nbytes, dtype=torch.uint8, device=dev).random_(0, 256)
+    sink = torch.zeros(1, dtype=torch.int64, device=dev)
+    ms = time_loop(lambda: fs.read_probe(buf, sink), iters, 3)
+    del buf
+    return {"gbs": round(nbytes / (ms * 1e-3) / 1e9, 1), "bytes": nbytes, "us_per_pass": round(ms * 1e3, 2),
+            "kernel": "read_probe_kernel (fs_read_probe: one CTA per SM, 6 x 32 KB cp.async.bulk ring)"}
+
+
 def stage1_time_ms(fs, fn, n):
     """Live CUDA events around each stage-1 launch inside the library (option time_stage1, which
     also disables PDL for those launches); average launch duration."""
@@ -587,6 +599,9 @@ def run_single(args):
     roof["timing"] = ("CUDA events over the K timed steps (one fused kernel per step, no PDL overlap)" if one_kernel
                       else "CUDA events around each stage-1 launch")
     roof["kernel_us_isolated"] = round(t1_ms * 1e3, 2)
+    rp = read_peak(fs, dev)
+    if roof["bound"] == "hbm":
+        roof["frac_of_read_peak"] = round(roof["achieved"] / rp["gbs"], 4)
     # end to end through the public API with host buffers: every step stages this step's h from pinned
     # host memory, samples, and the host reads the step's ids (stream sync per step, as a serving loop)
     h_host = wl["h"].cpu().pin_memory()
@@ -642,6 +657,7 @@ def run_single(args):
                               "previous step's kernel ends (PDL); a period, not a step latency",
             "hbm_gbs_achieved_step": round(algorithmic_bytes(B, D, V, transforms, n_groups) / (ms * 1e-3) / 1e9, 1),
             "roofline": roof,
+            "read_peak": rp,
             "clocks": clocks,
             "gpu_launches": (1 if one_kernel else 2) * args.steps * ((B + 255) // 256),
             "e2e": {"value": round(e2e_ms * 1e3, 2), "unit": UNIT, "h2d_bytes_per_step": h2d,

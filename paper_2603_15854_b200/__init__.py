@@ -355,6 +355,15 @@ def random_bits(seed: int, step: int, b: torch.Tensor, v: torch.Tensor, tag: int
     return r
 
 
+def read_probe(buf: torch.Tensor, sink: torch.Tensor, grid: int = 0) -> None:
+    """Read-only HBM roofline probe (fs_read_probe): stream the bytes of the device tensor `buf` once;
+    XOR of the first 8 bytes of every 32 KB chunk of each CTA slice into sink (int64 [1])."""
+    if not buf.is_cuda or not buf.is_contiguous() or sink.dtype != torch.int64 or not sink.is_cuda:
+        raise ValueError("buf: contiguous CUDA tensor; sink: CUDA int64 tensor")
+    _lib.check(_lib.lib().fs_read_probe(_ptr(buf), buf.numel() * buf.element_size(), _ptr(sink), int(grid),
+                                        _stream(buf)), "fs_read_probe")
+
+
 def gumbel_from_bits(r: torch.Tensor) -> torch.Tensor:
     """Device fp32 G32(r) (diagnostic, fs_gumbel_from_bits).  r: int32 tensor of bit patterns."""
     r = r.contiguous()

@@ -18,7 +18,7 @@ EXPORTS = [
     "fs_sample_logits_ex", "fs_sample_shard",
     "fs_combine_summaries", "fs_merge_summaries", "fs_random_bits", "fs_gumbel_from_bits",
     "fs_comm_window_create", "fs_comm_window_open", "fs_sample_tp_push", "fs_comm_window_destroy",
-    "fs_copy_async", "fs_sample_staged", "fs_comm_unique_id", "fs_comm_init", "fs_sample_tp", "fs_comm_destroy",
+    "fs_copy_async", "fs_sample_staged", "fs_read_probe", "fs_comm_unique_id", "fs_comm_init", "fs_sample_tp", "fs_comm_destroy",
 ]
 
 FS_OK, FS_ERR_INVALID, FS_ERR_UNSUPPORTED, FS_ERR_CUDA, FS_ERR_OOM, FS_ERR_NCCL = range(6)
@@ -78,6 +78,7 @@ def lib() -> ctypes.CDLL:
     L.fs_merge_summaries.argtypes = [vp, vp, vp, i32, vp]
     L.fs_random_bits.argtypes = [u64, u64, u32, vp, vp, vp, i64, vp]
     L.fs_gumbel_from_bits.argtypes = [vp, vp, i64, vp]
+    L.fs_read_probe.argtypes = [vp, ctypes.c_size_t, vp, i32, vp]
     L.fs_copy_async.argtypes = [vp, vp, vp, ctypes.c_size_t, vp]
     L.fs_sample_staged.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp, u64, u64, i32, i32, i32, vp, vp, vp]
     L.fs_comm_window_create.argtypes = [vp, i32, i32, i32, ctypes.POINTER(IpcHandle)]

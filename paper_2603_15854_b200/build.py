@@ -12,7 +12,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libflashsample.so")
-SOURCES = ["fs_api.cu", "fs_fused_tc.cu", "fs_fused_tc2.cu", "fs_fused_simt.cu", "fs_reduce.cu", "fs_logits.cu", "fs_topk.cu"]
+SOURCES = ["fs_api.cu", "fs_fused_tc.cu", "fs_fused_tc2.cu", "fs_fused_simt.cu", "fs_reduce.cu", "fs_logits.cu", "fs_topk.cu",
+           "fs_probe.cu"]
 HEADERS = ["fs_device.cuh", "fs_sm100.cuh", "fs_epilogue.cuh", "fs_kernels.h", "fs_peer.cuh", "fs_nccl.h",
            "fs_topk_epi.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -1297,6 +1297,21 @@ fs_status fs_copy_async(fs_ctx* ctx, void* dst, const void* src, size_t bytes, v
   return e == cudaSuccess ? FS_OK : cuda_fail(e, "copy kernel launch");
 }
 
+fs_status fs_read_probe(const void* src, size_t bytes, unsigned long long* sink, int grid, void* stream) {
+  if (bytes == 0) return FS_OK;
+  if (!src || !sink) return fail(FS_ERR_INVALID, "src and sink are required");
+  if ((reinterpret_cast<uintptr_t>(src) & 15u) || (bytes & 15u))
+    return fail(FS_ERR_INVALID, "src and bytes must be 16-byte aligned");
+  if (grid <= 0) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&grid, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return cuda_fail(e, "SM count");
+  }
+  cudaError_t e = fs::launch_read_probe(src, bytes, sink, grid, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? FS_OK : cuda_fail(e, "read probe launch");
+}
+
 fs_status fs_gumbel_from_bits(const uint32_t* r, float* g_out, int64_t n, void* stream) {
   if (n < 0 || (n > 0 && (!r || !g_out))) return fail(FS_ERR_INVALID, "r, g_out required");
   cudaError_t e = fs::launch_gumbel(r, g_out, n, static_cast<cudaStream_t>(stream));

@@ -548,7 +548,7 @@ def read_peak(fs, dev, nbytes=1 << 30, iters=20):
     ms = time_loop(lambda: fs.read_probe(buf, sink), iters, 3)
     del buf
     return {"gbs": round(nbytes / (ms * 1e-3) / 1e9, 1), "bytes": nbytes, "us_per_pass": round(ms * 1e3, 2),
-            "kernel": "read_probe_kernel (fs_read_probe: one CTA per SM, 6 x 32 KB cp.async.bulk ring)"}
+            "kernel": "read_probe_kernel (fs_read_probe: two CTAs per SM, each a 6 x 16 KB cp.async.bulk ring)"}
 
 
 def stage1_time_ms(fs, fn, n):

@@ -365,9 +365,9 @@ fs_status fs_random_bits(uint64_t seed, uint64_t step, uint32_t tag,
 fs_status fs_gumbel_from_bits(const uint32_t* r, float* g_out, int64_t n, void* stream);
 
 /* Read-only HBM roofline probe (a measured read-only peak next to the copy peak, which
- * counts read + write traffic).  `grid` CTAs (<= 0: one per SM) each stream a contiguous slice of the
+ * counts read + write traffic).  `grid` CTAs (<= 0: two per SM) each stream a contiguous slice of the
  * device buffer src[0, bytes) through a shared-memory ring with 1-D bulk copies (the TMA engine the
- * sampling kernels stream W with); the first 8 bytes of every 32 KB chunk of a slice (chunks counted
+ * sampling kernels stream W with); the first 8 bytes of every 16 KB chunk of a slice (chunks counted
  * from the slice start, slice = ceil(bytes / grid) rounded up to 16 bytes) are XOR-folded into *sink
  * (device, atomicXor), so no load is dead.  bench.py times it over 1 GiB.  FS_ERR_INVALID: NULL
  * pointers, src or bytes not 16-byte aligned.  Asynchronous on `stream`. */

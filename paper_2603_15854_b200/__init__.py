@@ -357,7 +357,7 @@ def random_bits(seed: int, step: int, b: torch.Tensor, v: torch.Tensor, tag: int
 
 def read_probe(buf: torch.Tensor, sink: torch.Tensor, grid: int = 0) -> None:
     """Read-only HBM roofline probe (fs_read_probe): stream the bytes of the device tensor `buf` once;
-    XOR of the first 8 bytes of every 32 KB chunk of each CTA slice into sink (int64 [1])."""
+    XOR of the first 8 bytes of every 16 KB chunk of each CTA slice into sink (int64 [1])."""
     if not buf.is_cuda or not buf.is_contiguous() or sink.dtype != torch.int64 or not sink.is_cuda:
         raise ValueError("buf: contiguous CUDA tensor; sink: CUDA int64 tensor")
     _lib.check(_lib.lib().fs_read_probe(_ptr(buf), buf.numel() * buf.element_size(), _ptr(sink), int(grid),

@@ -1307,6 +1307,7 @@ fs_status fs_read_probe(const void* src, size_t bytes, unsigned long long* sink,
     cudaError_t e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&grid, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return cuda_fail(e, "SM count");
+    grid *= 2;                                  // two CTAs (rings) per SM
   }
   cudaError_t e = fs::launch_read_probe(src, bytes, sink, grid, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? FS_OK : cuda_fail(e, "read probe launch");

@@ -1,9 +1,10 @@
 // fs_probe.cu -- read-only HBM roofline probe ("a measured read-only peak (a 1 GiB
 // bf16 read-reduction kernel), because the copy peak counts read+write traffic").
 //
-// Every CTA of a persistent grid streams one contiguous slice of `src` into a shared-memory ring with
-// 1-D bulk copies (cp.async.bulk: the TMA engine the sampling kernels stream W with, minus the tensor
-// map), 32 KB per stage, six stages in flight; one consumer thread folds the first 8 bytes of every
+// Every CTA of a persistent grid (two per SM) streams one contiguous slice of `src` into a shared-
+// memory ring with 1-D bulk copies (cp.async.bulk: the TMA engine the sampling kernels stream W with,
+// minus the tensor map), 16 KB per stage, six stages in flight (the fastest geometry of the sweep in
+// profiles/r02/read_probe_geometry.log); one consumer thread folds the first 8 bytes of every
 // chunk into an XOR (so no load is dead) and frees the stage.  bench.py divides the bytes by the
 // launch time: the ceiling a pure W stream can reach on this GPU, next to the copy peak of
 // MEASURED_PEAKS.json.
@@ -17,7 +18,7 @@
 namespace fs {
 
 namespace {
-constexpr int kProbeChunk = 32768;
+constexpr int kProbeChunk = 16384;
 constexpr int kProbeStages = 6;
 
 __device__ __forceinline__ void bulk_load(void* smem_dst, const void* src, uint32_t bytes, uint64_t* bar,
@@ -32,7 +33,7 @@ __device__ __forceinline__ void bulk_load(void* smem_dst, const void* src, uint3
 
 // Slice of CTA c: [c * per, min(bytes, (c + 1) * per)), per = ceil(bytes / G) rounded up to 16 bytes;
 // chunks of kProbeChunk bytes from the slice start (the last one shorter).
-__global__ void __launch_bounds__(64, 1) read_probe_kernel(const uint8_t* __restrict__ src, size_t bytes,
+__global__ void __launch_bounds__(64, 2) read_probe_kernel(const uint8_t* __restrict__ src, size_t bytes,
                                                            unsigned long long* sink) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* ring = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);

@@ -1,5 +1,5 @@
 """GPU: the read-only roofline probe (fs_read_probe) reads every chunk it claims to: its XOR fold of the
-first 8 bytes of every 32 KB chunk of each CTA slice equals the same fold computed on the host."""
+first 8 bytes of every 16 KB chunk of each CTA slice equals the same fold computed on the host."""
 import numpy as np
 import pytest
 import torch
@@ -16,7 +16,7 @@ def _host_fold(buf: np.ndarray, grid: int) -> int:
     acc = 0
     for c in range(grid):
         lo, hi = min(n, per * c), min(n, per * c + per)
-        for off in range(lo, hi, 32768):
+        for off in range(lo, hi, 16384):
             acc ^= int(buf[off:off + 8].view(np.uint64)[0])
     return acc
 
@@ -29,7 +29,7 @@ def test_read_probe_reads_every_chunk(nbytes, grid):
     sink = torch.zeros(1, dtype=torch.int64, device="cuda")
     fs.read_probe(buf, sink, grid)
     torch.cuda.synchronize()
-    G = grid if grid > 0 else torch.cuda.get_device_properties(0).multi_processor_count
+    G = grid if grid > 0 else 2 * torch.cuda.get_device_properties(0).multi_processor_count
     assert int(sink.cpu().numpy().view(np.uint64)[0]) == _host_fold(host.numpy(), G)
 
 

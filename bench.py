@@ -699,11 +699,13 @@ def sweep(fs, name, pk, args, Bs=SWEEP_B):
         with ClockSampler(0) as clk_loop:
             loop_us = 1e3 * time_loop(fn, 100, 10)      # back-to-back steps, no overlap (as the headline)
         t1 = stage1_time_ms(fs, fn, 50)
-        fs.set_option("pdl_w", 1)
-        pipe_us = 1e3 * time_loop(fn, 100, 10)          # PDL-pipelined period
-        fs.set_option("pdl_w", 0)
+        pipe_us = None                                  # pdl_w = 1 applies PDL only up to pdl_w_max_b = 128 rows
+        if B <= 128:
+            fs.set_option("pdl_w", 1)
+            pipe_us = round(1e3 * time_loop(fn, 100, 10), 2)   # PDL-pipelined period
+            fs.set_option("pdl_w", 0)
         r = {"fused_us": round(us, 2), "fused_p10_p90_us": [round(q10, 2), round(q90, 2)],
-             "fused_loop_us": round(loop_us, 2), "pipelined_us": round(pipe_us, 2),
+             "fused_loop_us": round(loop_us, 2), "pipelined_us": pipe_us,
              "stage1_us": round(t1 * 1e3, 2), "one_kernel": one_kernel,
              "clocks": {k: {"sm_mhz": c.get("sm_mhz"), "power_w": c.get("power_w_median"), "reasons": c.get("reasons")}
                         for k, c in (("call", clk_call.summary()), ("loop", clk_loop.summary()))}}

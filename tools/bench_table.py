@@ -15,7 +15,7 @@ for cname, sw in sweeps:
     for k, v in sw.items():
         bl = v.get("baselines", {})
         ro = v["roofline"]
-        print(f"| {cname} | {k[1:]} | {v['fused_us']:.1f} | {v['fused_loop_us']:.1f} | {v['pipelined_us']:.1f} | "
+        print(f"| {cname} | {k[1:]} | {v['fused_us']:.1f} | {v['fused_loop_us']:.1f} | {('%.1f' % v['pipelined_us']) if v.get('pipelined_us') is not None else '— (no PDL at B > 128)'} | "
               f"{ro['bound']} {ro['frac']:.3f} ({ro['frac_of_floor']:.3f}) | {bl.get('cublas_gemm_only_us', 0):.1f} | "
               f"{bl.get('multinomial_eager_us', 0):.1f} / {bl.get('multinomial_compiled_us', 0):.1f} | "
               f"{bl.get('fi2_gemm_sampling_from_logits_us', 0):.1f} | {bl.get('fi1_gemm_top_k_top_p_us', 0):.1f} | "

@@ -24,7 +24,7 @@ block = f"""r02 results (`profiles/r02/bench.json`, the final evidence run of ro
 active in {c.get('reason_samples', {}).get('sw_power_cap', 0)} of {c['samples']} clock samples of the headline window; µs per step). "per call" = median
 of 100 individually event-timed calls after 25 warm-ups (the paper's protocol); "loop" = 100
 back-to-back steps without cross-step overlap (the headline's protocol); "pipelined" = back-to-back
-with `pdl_w` = 1; frac = achieved / peak of the binding roofline (HBM copy peak, or sustained bf16
+with `pdl_w` = 1 (PDL applies up to B = 128, `pdl_w_max_b`); frac = achieved / peak of the binding roofline (HBM copy peak, or sustained bf16
 tensor peak), in brackets against max(t_HBM, t_TC); "×" = best unfused baseline (or cuBLAS GEMM
 alone) ÷ our per-call time. Box-to-box spread under the power cap is several % (B ≥ 128 rows
 especially: the loop column runs at the sustained power limit).

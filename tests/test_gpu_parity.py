@@ -101,6 +101,22 @@ def test_degenerate_single_token_vocab():
     check_flat(idx, score, flat)
 
 
+@pytest.mark.parametrize("V,D,B,pair", [(2, 8, 1, 0), (7, 16, 17, 1), (127, 8, 33, 1), (128, 24, 3, 0),
+                                        (129, 8, 64, 1), (255, 16, 2, 0), (256, 8, 100, 1), (257, 24, 256, 1),
+                                        (383, 8, 16, 0), (513, 16, 31, -1)])
+def test_tiny_vocab_and_width_around_tile_boundaries(V, D, B, pair):
+    # smallest TMA-legal widths (D = 8 bf16 = 16 B rows) and V around the 128 / 256-row tile edges, on
+    # the 1-CTA and the CTA-pair kernel; whole-tile and 16-row partitions agree bit for bit
+    wl = synth.make_workload("qwen25_7b", B, V=V, D=D, seed_offset=V * 3 + D)
+    fs.set_option("pair", pair)
+    idx, score = _run(wl, 1)
+    _, flat = oracle_flat(wl, 1)
+    check_flat(idx, score, flat)
+    fs.set_option("whole_tiles", 0)
+    idx2, score2 = _run(wl, 1)
+    assert np.array_equal(idx, idx2) and np.array_equal(score.view(np.uint32), score2.view(np.uint32))
+
+
 def test_invalid_temperature_rows():
     wl = synth.make_workload("llama3_8b", 4, V=500, D=64)
     wl.temperature = torch.tensor([1.0, -0.5, -1.0, float("nan")])

@@ -189,18 +189,23 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
       int stage = 0;
       uint32_t phase = 0;
       int tile_i = 0;
+      uint64_t wait_acc = 0, wait_data = 0;   // debug (dbg_times): ns the MMA issuer waited
       for (int a = r0; a < r1;) {
         const int b = seg_end(a, r1, gs);
         const int T = seg_tile_rows(b - a, kBlockM, kTileGran);
         for (int t0 = a; t0 < b; t0 += T, ++tile_i) {
           const int buf = tile_i & 1;
           const uint32_t use = (uint32_t)(tile_i >> 1);
+          const uint64_t tw0 = p.dbg_times ? sm100::globaltimer() : 0;
           sm100::mbar_wait(&tempty[buf], (use & 1) ^ 1);
+          if (p.dbg_times) wait_acc += sm100::globaltimer() - tw0;   // MMA idle: accumulator not drained
           sm100::tc_fence_after();
           const uint32_t d_tmem = tmem_base + (uint32_t)(buf * BN);
           for (int kb0 = 0; kb0 < num_kb; kb0 += KBPS) {
             const int nk = p.dbg_no_mma == 1 ? 0 : min(KBPS, num_kb - kb0);
+            const uint64_t fw0 = p.dbg_times ? sm100::globaltimer() : 0;
             sm100::mbar_wait(&full[stage], phase);
+            if (p.dbg_times) wait_data += sm100::globaltimer() - fw0;   // MMA idle: operands not landed
             sm100::tc_fence_after();
             for (int j = 0; j < nk; ++j) {
               const uint64_t adesc =
@@ -217,6 +222,10 @@ fused_tc_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p)
           sm100::mma_commit(&tfull[buf]);
         }
         a = b;
+      }
+      if (p.dbg_times) {
+        p.dbg_times[blockIdx.x * 8 + 6] = wait_acc;
+        p.dbg_times[blockIdx.x * 8 + 7] = wait_data;
       }
     }
   } else if constexpr (MODE == 1) {

@@ -101,7 +101,8 @@ struct StageOneParams {
   float* logprob_out;             // [B] or nullptr
   int need_lt;                    // some output of the call reads the winner's l~ (log-prob)
   unsigned long long* dbg_times;  // debug: [grid][8] globaltimer ns (start, dependency wait done, last load
-                                  // issued, last tile drained), %smid, CTA done, 0, 0; or nullptr
+                                  // issued, last tile drained), %smid, CTA done, and the MMA issuer's total
+                                  // ns waiting for a drained accumulator / for operands (MMA CTAs); or nullptr
   const void* h_host;             // in-kernel staging (fs_sample_staged): pinned host h copied into h by
                                   // all CTAs after the dependency wait, then a grid barrier (h_bar)
                                   // before the first h load; nullptr = h is already on the device

@@ -635,8 +635,11 @@ def run_single(args):
         prepared.wait()
         sink[0] += int(idx_np[0])
     # the host syncs every step, so nothing overlaps across steps; pdl_w = 1 only lets this step's
-    # W stream start while the kernel itself is still staging h from host memory
+    # W stream start while the kernel itself is still staging h from host memory (the prepared
+    # sampler has a context of its own: the option is set on it too)
     fs.set_option("pdl_w", 1)
+    if prepared is not None:
+        prepared.set_option("pdl_w", 1)
     e2e_ms = time_loop(e2e_prepared if prepared else e2e_generic, args.steps, args.warmup)
     e2e_generic_ms = time_loop(e2e_generic, args.steps, args.warmup) if prepared else e2e_ms
     fs.set_option("pdl_w", 0)

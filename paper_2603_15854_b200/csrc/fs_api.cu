@@ -256,7 +256,7 @@ fs_status segment_maps(fs_ctx* ctx, const void* W, int64_t D, int V, int G, int 
       const int b = std::min(r1, (a / gs + 1) * gs);
       const cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)(b - a)};
       const cuuint64_t strides[1] = {(cuuint64_t)D * 2};
-      const int T = pair ? fs::seg_tile_rows(b - a, 256, 16) / 2 : fs::seg_tile_rows(b - a, 128, gran);
+      const int T = pair ? fs::seg_tile_rows(b - a, 256, std::max(16, gran)) / 2 : fs::seg_tile_rows(b - a, 128, gran);
       const cuuint32_t box[2] = {64u, (cuuint32_t)T};
       const cuuint32_t estr[2] = {1u, 1u};
       CUresult r = ctx->encode(&maps[(size_t)c * max_seg + s], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
@@ -574,8 +574,16 @@ fs_status run_topk_path(fs_ctx* ctx, const PathArgs& a, int k, float top_p, cuda
   }
   const CUtensorMap* wmaps = nullptr;
   int max_seg = 1;
+  // raw-logit route on the CTA-pair kernel (M = 256, each CTA loads half of h; pair tiles in 32-row
+  // units so that every CTA half starts on a 16-row span unit) above B = 128, where halving the h
+  // traffic pays (measured per call, k = 50: B = 256 360 -> 329 us; B = 64 / 128 no gain);
+  // option pair = 1 forces it from the pair batch size on
+  const bool pair2 = tc && !lists && a.B <= chunk && ctx->pair != 0 && G >= 2 &&
+                     (ctx->pair == 1 ? BN_max >= ctx->pair_min_bn : BN_max > 128);
+  const int G2 = pair2 ? (G / 2) * 2 : G;
   if (tc) {
-    fs_status st0 = segment_maps(ctx, a.W, a.D, a.V, G, unit, a.V, &wmaps, &max_seg, 0, 16);   // top-k modes
+    fs_status st0 = pair2 ? segment_maps(ctx, a.W, a.D, a.V, G2 / 2, unit, a.V, &wmaps, &max_seg, 1, 32)
+                          : segment_maps(ctx, a.W, a.D, a.V, G, unit, a.V, &wmaps, &max_seg, 0, 16);   // top-k modes
     if (st0 != FS_OK) return st0;
   }
   // workspace: candidates [Bc][G*k] (lists) or logits [Bc][V] fp32 + chunk candidates
@@ -630,6 +638,17 @@ fs_status run_topk_path(fs_ctx* ctx, const PathArgs& a, int k, float top_p, cuda
       p.w_policy = ctx->w_policy;
       p.dbg_no_epi = ctx->dbg_no_epi;
       p.dbg_no_mma = ctx->dbg_no_mma;
+      if (pair2) {
+        p.kbps = 1;
+        for (int kk = 4; kk >= 2; --kk)
+          if (fs::tc2_stages(BN, kk) >= 3) { p.kbps = kk; break; }
+        p.stages = fs::tc2_stages(BN, p.kbps);
+        CUtensorMap hmap;
+        if ((st = make_map(ctx, &hmap, p.h, a.D, Bc, BN / 2)) != FS_OK) return st;
+        p.wmaps = wmaps;
+        e = fs::launch_fused_tc2_raw(hmap, p, BN, G2, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "stage-1 tcgen05 pair raw-logit kernel launch");
+      } else {
       const int ex = lists ? fs::tc_topk_extra_bytes(BN, cap) : 0;
       p.kbps = 0;
       for (int kk = 4; kk >= 2; --kk)
@@ -649,6 +668,7 @@ fs_status run_topk_path(fs_ctx* ctx, const PathArgs& a, int k, float top_p, cuda
       p.wmaps = wmaps;
       e = fs::launch_fused_tc_topk(hmap, p, BN, G, stream);
       if (e != cudaSuccess) return cuda_fail(e, "stage-1 top-k kernel launch");
+      }
     } else {
       e = fs::launch_fused_simt(p, a.dtype, false, stream);
       if (e != cudaSuccess) return cuda_fail(e, "stage-1 CUDA-core logits kernel launch");

@@ -22,6 +22,7 @@
 
 #include "fs_epilogue.cuh"
 #include "fs_kernels.h"
+#include "fs_topk_epi.cuh"
 
 namespace fs {
 
@@ -41,7 +42,10 @@ int tmem_cols_for(int BN) {
 __device__ __forceinline__ int seg_end2(int a, int r1, int gs) { return min(r1, (a / gs + 1) * gs); }
 }  // namespace
 
-template <bool LSE, bool XFORM, bool PRQ>
+// MODE 0: sampling epilogue; MODE 2: raw fp32 logits + per-32-row span maxima for the fused top-k
+// raw-logit route (fs_topk.cu gathers the spans at or above the k-th largest), as the 1-CTA kernel's
+// mode 2 -- pair tiles are then cut in 32-row units so every CTA half starts on a 16-row span unit.
+template <bool LSE, bool XFORM, bool PRQ, int MODE = 0>
 __global__ void __launch_bounds__(kThreads, 1)   // 18 warps: <= 96 registers (5 warps on a 16K-register SM sub-partition)
 fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -49,6 +53,7 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
   // from it stays in the shared address space (LDS/STS/ATOMS, not generic LD/ST)
   uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
   const int S = p.stages, BN = p.bn, KBPS = p.kbps;
+  constexpr int kGran = MODE == 2 ? 32 : 16;                  // pair tile granularity (rows)
   const int h_bytes = (BN / 2) * kBlockK * 2;                 // this CTA's half of h per K slice
   uint8_t* w_ring = smem;
   uint8_t* h_ring = smem + (size_t)S * KBPS * kWBytes;
@@ -137,7 +142,7 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
       for (int a = r0; a < r1; ++seg) {
         const int b = seg_end2(a, r1, gs);
         const CUtensorMap* wm = &wmaps[seg];
-        const int T2 = seg_tile_rows(b - a, 256, 16), Th = T2 / 2;   // pair tile, this CTA's half
+        const int T2 = seg_tile_rows(b - a, 256, kGran), Th = T2 / 2;   // pair tile, this CTA's half
         const uint32_t pair_tx = 2u * (uint32_t)(Th * kBlockK * 2 + h_bytes);
         for (int t0 = a; t0 < b; t0 += T2) {
           for (int kb0 = 0; kb0 < num_kb; kb0 += KBPS) {
@@ -176,7 +181,7 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
       uint64_t wait_acc = 0, wait_data = 0;   // debug (dbg_times): ns the MMA issuer waited
       for (int a = r0; a < r1;) {
         const int b = seg_end2(a, r1, gs);
-        const int T2 = seg_tile_rows(b - a, 256, 16);
+        const int T2 = seg_tile_rows(b - a, 256, kGran);
         for (int t0 = a; t0 < b; t0 += T2, ++tile_i) {
           const int buf = tile_i & 1;
           const uint32_t use = (uint32_t)(tile_i >> 1);
@@ -212,6 +217,32 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
         p.dbg_times[blockIdx.x * 8 + 7] = wait_data;
       }
     }
+  } else if constexpr (MODE == 2) {
+    // ------------------------ raw logits + span maxima (both CTAs) ----------------------
+    const int e = warp - 2;
+    const int set = e >> 3;
+    const int half = (e >> 2) & 1;                  // columns 8*half, 8*half + 16, ...
+    const int q = warp & 3;
+    const uint32_t tempty_leader = sm100::mapa(sm100::smem_u32(&tempty[set]), 0);
+    int tile_i = 0;
+    for (int a = r0; a < r1;) {
+      const int b = seg_end2(a, r1, gs);
+      const int T2 = seg_tile_rows(b - a, 256, kGran), Th = T2 / 2;
+      for (int t0 = a; t0 < b; t0 += T2, ++tile_i) {
+        if ((tile_i & 1) != set) continue;
+        const uint32_t use = (uint32_t)(tile_i >> 1);
+        sm100::mbar_wait(&tfull[set], use & 1);
+        sm100::tc_fence_after();
+        const int base = t0 + Th * (int)rank;
+        const int hi = min(b, base + Th);
+        const int row = base + 32 * q + lane, span0 = base + 32 * q;
+        const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(set * BN);
+        epi_tile_store(taddr, row < hi, row, p.B, p.mat_out, p.mat_ld, p.topk_gmax, p.topk_gld, span0 >> 4,
+                       max(0, min(32, hi - span0)), lane, 8 * half, 16);
+        release_tmem(&tempty[set], tempty_leader, lane);
+      }
+      a = b;
+    }
   } else {
     // -------------------------------- epilogue (both CTAs) ------------------------------
     const int e = warp - 2;
@@ -240,7 +271,7 @@ fused_tc2_kernel(const __grid_constant__ CUtensorMap tmH, const StageOneParams p
     int tile_i = 0, seg = 0;
     for (int a = r0; a < r1; ++seg) {
       const int b = seg_end2(a, r1, gs);
-      const int T2 = seg_tile_rows(b - a, 256, 16), Th = T2 / 2;
+      const int T2 = seg_tile_rows(b - a, 256, kGran), Th = T2 / 2;
       for (int t0 = a; t0 < b; t0 += T2, ++tile_i) {
         if ((tile_i & 1) != set) continue;
         const uint32_t use = (uint32_t)(tile_i >> 1);
@@ -351,6 +382,20 @@ static cudaLaunchConfig_t tc2_config(const StageOneParams& p, int BN, int grid, 
   cfg.attrs = attr;
   cfg.numAttrs = p.pdl_w ? 2 : 1;
   return cfg;
+}
+
+cudaError_t launch_fused_tc2_raw(const CUtensorMap& hmap, const StageOneParams& p_in, int BN, int grid,
+                                 cudaStream_t stream) {
+  StageOneParams p = p_in;
+  p.bn = BN;
+  p.tmem_cols = tmem_cols_for(BN);
+  p.pdl_w = 0;
+  auto kern = fused_tc2_kernel<false, false, false, 2>;
+  cudaError_t e = ensure_smem_attr(reinterpret_cast<const void*>(kern), 227 * 1024);
+  if (e != cudaSuccess) return e;
+  cudaLaunchAttribute attr[2];
+  cudaLaunchConfig_t cfg = tc2_config(p, BN, grid, stream, attr);
+  return cudaLaunchKernelEx(&cfg, kern, hmap, p);
 }
 
 cudaError_t fused_tc2_resident(const StageOneParams& p, int BN, bool lse, int grid, int* ctas) {

@@ -202,6 +202,8 @@ cudaError_t launch_combine(const fs_summary* gathered, int n, int B, int32_t* id
                            float* logZ_out, cudaStream_t stream);
 cudaError_t launch_merge(const fs_summary* a, const fs_summary* b, fs_summary* out, int count,
                          cudaStream_t stream);
+cudaError_t launch_fused_tc2_raw(const CUtensorMap& hmap, const StageOneParams& p, int BN, int grid,
+                                 cudaStream_t stream);
 cudaError_t launch_read_probe(const void* src, size_t bytes, unsigned long long* sink, int grid, cudaStream_t stream);
 cudaError_t launch_random_bits(uint64_t seed, uint64_t step, uint32_t tag, const int32_t* b, const int64_t* v,
                                uint32_t* r, int64_t n, cudaStream_t stream);

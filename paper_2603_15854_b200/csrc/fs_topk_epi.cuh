@@ -263,9 +263,10 @@ __device__ __forceinline__ void topk_write_cols(const TopkSmem& ts, int B, int q
 // gmax[col][u0] and the marker 1 to gmax[col][u0 + 1] when the span covers a second 16-row unit.
 __device__ __forceinline__ void epi_tile_store(uint32_t taddr, bool valid, int row, int B, float* out, int64_t ld,
                                                uint32_t* gmax = nullptr, int64_t gld = 0, int64_t u0 = 0,
-                                               int span_rows = 0, int lane = 0) {
+                                               int span_rows = 0, int lane = 0, int col_first = 0,
+                                               int col_step = 8) {
 #pragma unroll 1
-  for (int col0 = 0; col0 < B; col0 += 8) {
+  for (int col0 = col_first; col0 < B; col0 += col_step) {
     uint32_t r[8];
     sm100::tmem_ld_32x32b_x8(taddr + (uint32_t)col0, r);
     sm100::tmem_wait_ld();

@@ -29,6 +29,7 @@ def _reset():
         fs.set_option("force_simt", 0)
         fs.set_option("max_ctas", 0)
         fs.set_option("topk_spans", 1)
+        fs.set_option("pair", -1)
 
 
 def _dev(t):
@@ -223,3 +224,20 @@ def test_raw_route_span_gather_all_ties():
     W = torch.zeros(V, D, dtype=torch.bfloat16).cuda()
     idx = fs.sample(h, W, seed=1, step=2, top_k=k)
     assert bool((idx.cpu() < k).all()) and bool((idx.cpu() >= 0).all())
+
+
+@pytest.mark.parametrize("B,V", [(17, 4099), (64, 20011), (128, 9000), (256, 5003)])
+def test_raw_route_pair_kernel_equals_single_cta(B, V):
+    # raw-logit route on the CTA-pair kernel (32-row pair tile units, span maxima per CTA half) vs the
+    # 1-CTA kernel: the same stored logits and span bounds, hence identical samples; and the oracle
+    fs.set_option("topk_mode", 2)
+    wl = synth.make_workload("llama3_8b", B, V=V, D=192, seed_offset=3 * B + 1, pattern="peaked")
+    out = {}
+    for pair in (0, 1):                       # 1 forces the pair kernel from B = 17 (auto: B > 128)
+        fs.set_option("pair", pair)
+        out[pair] = _run(wl, 50, 0.95, step=5)
+    fs.set_option("pair", -1)
+    for a, b in zip(out[0], out[1]):
+        assert torch.equal(a.view(torch.int32), b.view(torch.int32))
+    _, res = _oracle(wl, 50, 0.95, step=5)
+    _check(out[1][0], out[1][1], res)

@@ -10,6 +10,7 @@ echo "pytest rc=$?" >> "$OUT/pytest_gpu.log"
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/smoke.log" 2>&1
 echo "smoke rc=$?" >> "$OUT/smoke.log"
 if [ -z "${NO_BENCH:-}" ]; then
+  t0=$(date +%s)
   timeout ${BENCH_TIMEOUT:-900} python bench.py ${BENCH_ARGS:-} > "$OUT/bench.log" 2>&1
-  echo "bench rc=$?" >> "$OUT/bench.log"
+  echo "bench rc=$? wall_s=$(( $(date +%s) - t0 ))" >> "$OUT/bench.log"
 fi

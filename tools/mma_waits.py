@@ -35,7 +35,8 @@ for B in Bs:
     A = np.stack([b.cpu().numpy().reshape(148, 8) for b in bufs]).astype(np.float64)
     G = int((A[0, :, 0] > 0).sum())
     A = A[:, :G]
-    dur = (A[:, :, 5].max(1) - A[:, :, 0].min(1)) / 1e3                  # kernel span, us
+    end = np.where(A[:, :, 5] > 0, A[:, :, 5], A[:, :, 3])                 # CTA done, else last tile drained
+    dur = (end.max(1) - A[:, :, 0].min(1)) / 1e3                          # kernel span, us
     mma = A[:, :, 6] + A[:, :, 7] > 0                                       # CTAs that issue MMAs
     acc = np.array([A[s, mma[s], 6].mean() for s in range(n)]) / 1e3
     dat = np.array([A[s, mma[s], 7].mean() for s in range(n)]) / 1e3

@@ -590,8 +590,11 @@ topk_final_kernel(const Cand* __restrict__ cand, int ncand, int* __restrict__ ro
 // logit is >= T); relaxed by 8 key steps so that an element whose transformed value ties the k-th
 // after fp32 rounding of l/tau is still gathered.  Only the spans at or above it are read back.
 constexpr int kGatherThreads = 1024;
-constexpr int kGatherPer = 32;            // span entries per thread: V <= 16 * 1024 * 32
-__global__ void __launch_bounds__(kGatherThreads)
+constexpr int kGatherPer = 32;            // most span entries per thread: V <= 16 * 1024 * 32
+// PER span entries per thread (8 / 16 / 32 by V): fewer registers for V <= 262,144, so
+// that two 1024-thread blocks (rows) fit on an SM (B = 256 in one wave)
+template <int PER>
+__global__ void __launch_bounds__(kGatherThreads, PER <= 16 ? 2 : 1)
 topk_gather_kernel(const float* __restrict__ mat, int64_t ld, const uint32_t* __restrict__ gmax, int64_t gld,
                    const float* __restrict__ temperature, int V, int k, Cand* __restrict__ cand, int64_t stride,
                    int* __restrict__ row_count) {
@@ -600,10 +603,10 @@ topk_gather_kernel(const float* __restrict__ mat, int64_t ld, const uint32_t* __
   const int b = blockIdx.x;
   const int64_t nunits = (V + 15) / 16;
   const uint32_t* g = gmax + (int64_t)b * gld;
-  uint32_t keys[kGatherPer];
-  bool valid[kGatherPer];
+  uint32_t keys[PER];
+  bool valid[PER];
 #pragma unroll
-  for (int j = 0; j < kGatherPer; ++j) {
+  for (int j = 0; j < PER; ++j) {
     const int64_t u = threadIdx.x + (int64_t)j * kGatherThreads;
     keys[j] = u < nunits ? g[u] : 0u;
     valid[j] = keys[j] > 1u;               // 0 / 1: no span starts at this unit
@@ -613,7 +616,7 @@ topk_gather_kernel(const float* __restrict__ mat, int64_t ld, const uint32_t* __
   // so k elements are >= it (a 1-key-per-thread select instead of 32)
   uint32_t tmax = 0u;
 #pragma unroll
-  for (int j = 0; j < kGatherPer; ++j) tmax = valid[j] && keys[j] > tmax ? keys[j] : tmax;
+  for (int j = 0; j < PER; ++j) tmax = valid[j] && keys[j] > tmax ? keys[j] : tmax;
   const bool tvalid = tmax > 1u;
   uint32_t T = 0;
   int take = 0;
@@ -626,26 +629,33 @@ topk_gather_kernel(const float* __restrict__ mat, int64_t ld, const uint32_t* __
   }
   const float* row = mat + (int64_t)b * ld;
   Cand* out = cand + (int64_t)b * stride;
+  // the spans to read back as a bit mask (keys / valid stay in registers: they are only indexed in
+  // unrolled loops; a rolled loop over them compiled to local-memory arrays)
+  uint32_t sel = 0u;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) sel |= (valid[j] && keys[j] >= Tr) ? (1u << j) : 0u;
 #pragma unroll 1
-  for (int j = 0; j < kGatherPer; ++j) {
-    if (!valid[j] || keys[j] < Tr) continue;
+  for (; sel != 0u; sel &= sel - 1u) {
+    const int j = __ffs(sel) - 1;
     const int64_t u = threadIdx.x + (int64_t)j * kGatherThreads;
     const int64_t v0 = u * 16;
     const int64_t want = (u + 1 < nunits && g[u + 1] == 1u) ? 32 : 16;
     const int n = (int)(want < V - v0 ? want : V - v0);
-    float x[32];
+#pragma unroll 1
+    for (int i0 = 0; i0 < n; i0 += 8) {             // 8 loads in flight per round (few registers)
+      float x[8];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) x[i] = i < n ? row[v0 + i] : -INFINITY;
+      for (int i = 0; i < 8; ++i) x[i] = i0 + i < n ? row[v0 + i0 + i] : -INFINITY;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      if (i >= n) break;
-      float raw = x[i];
-      if (isnan(raw)) raw = -INFINITY;
-      if (order_key(raw) < Tr) continue;
-      float l = raw * it;
-      if (isnan(l)) l = -INFINITY;
-      const int pos = atomicAdd(&cnt, 1);
-      out[pos] = Cand{order_key(l), (int32_t)(v0 + i)};
+      for (int i = 0; i < 8; ++i) {
+        float raw = x[i];
+        if (isnan(raw)) raw = -INFINITY;
+        if (i0 + i >= n || order_key(raw) < Tr) continue;
+        float l = raw * it;
+        if (isnan(l)) l = -INFINITY;
+        const int pos = atomicAdd(&cnt, 1);
+        out[pos] = Cand{order_key(l), (int32_t)(v0 + i0 + i)};
+      }
     }
   }
   __syncthreads();
@@ -659,9 +669,17 @@ int topk_chunks(int V) { return (V + kChunk - 1) / kChunk; }
 cudaError_t launch_topk_gather(const float* mat, int64_t ld, const uint32_t* gmax, int64_t gld,
                                const float* temperature, int B, int V, int k, Cand* cand, int64_t stride,
                                int* row_count, cudaStream_t stream) {
-  if ((int64_t)(V + 15) / 16 > (int64_t)kGatherThreads * kGatherPer) return cudaErrorInvalidValue;
-  topk_gather_kernel<<<B, kGatherThreads, 0, stream>>>(mat, ld, gmax, gld, temperature, V, k, cand, stride,
-                                                        row_count);
+  const int64_t units = (int64_t)(V + 15) / 16;
+  if (units > (int64_t)kGatherThreads * kGatherPer) return cudaErrorInvalidValue;
+  if (units <= (int64_t)kGatherThreads * 8)
+    topk_gather_kernel<8><<<B, kGatherThreads, 0, stream>>>(mat, ld, gmax, gld, temperature, V, k, cand, stride,
+                                                            row_count);
+  else if (units <= (int64_t)kGatherThreads * 16)
+    topk_gather_kernel<16><<<B, kGatherThreads, 0, stream>>>(mat, ld, gmax, gld, temperature, V, k, cand, stride,
+                                                             row_count);
+  else
+    topk_gather_kernel<32><<<B, kGatherThreads, 0, stream>>>(mat, ld, gmax, gld, temperature, V, k, cand, stride,
+                                                             row_count);
   return cudaGetLastError();
 }
 int topk_max_k() { return kMaxK; }

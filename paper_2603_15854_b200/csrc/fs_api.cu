@@ -559,13 +559,16 @@ fs_status run_topk_path(fs_ctx* ctx, const PathArgs& a, int k, float top_p, cuda
   const int slices = tc ? ring_slices(BN_max, extra) : 0;
   if (ctx->topk_mode == 1 && slices < 2)
     return fail(FS_ERR_UNSUPPORTED, "top-k candidate lists do not fit in shared memory for this B and k (topk_mode=1)");
-  // auto: lists for k <= 128 when the ring keeps >= 8 slices (measured, DESIGN.md §11: at k = 200 the
-  // per-tile compactions cost more than the raw-logit round trip)
-  const bool lists = ctx->topk_mode == 1 || (ctx->topk_mode == 0 && slices >= 8 && k <= 128);
   // raw-logit route with span maxima (stage 1 also writes per-32-row maxima; only the spans at or
   // above the k-th largest are read back): needs the tcgen05 kernel and no bias / mask (the bound is
   // taken on raw logits, valid under the monotone temperature transform)
-  const bool spans = !lists && tc && ctx->topk_spans && !a.bias && !a.mask && (a.V + 15) / 16 <= 32768;
+  const bool spans_ok = tc && ctx->topk_spans && !a.bias && !a.mask && (a.V + 15) / 16 <= 32768;
+  // auto: lists for k <= 128 when the ring keeps >= 8 slices (measured, DESIGN.md §11: at k = 200 the
+  // per-tile compactions cost more than the raw-logit round trip), and -- where the span route is
+  // available -- only up to B = 16: from B = 32 the span route is faster (§11 entry 36)
+  const bool lists = ctx->topk_mode == 1 ||
+                     (ctx->topk_mode == 0 && slices >= 8 && k <= 128 && (BN_max <= 16 || !spans_ok));
+  const bool spans = !lists && spans_ok;
   if ((lists || spans) && !ctx->topk_rowcnt) {
     e = cudaMalloc(&ctx->topk_rowcnt, 256 * sizeof(int));
     if (e != cudaSuccess) return fail(FS_ERR_OOM, std::string("row counter cudaMalloc failed: ") + cudaGetErrorString(e) + kAllocHint);
